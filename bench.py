@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Throughput of the FP64 matrix-free elasticity apply y = A x on B200 (GDoF/s per apply).
+
+Default workload: BASELINE.json config 5 (64x64x256 Q6, q=8, perturbed trilinear geometry,
+per-element LogNormal(0,0.5) material, 683,465,475 DoF) -- the largest configuration that
+fits one GPU and the one the multi-GPU (z-slab) runs use.  With N=1 the line also carries
+the config-4 p-sweep (p = 1..8 at ~50M DoF, the metric's "vs p=1..8").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+A step = one elas_apply over the whole (rank-local) mesh: init kernel + fused apply kernel
+(+ interface exchange for N > 1).  Timing: CUDA events on the op's stream over exactly K
+steps, bracketed by barrier + synchronize, max over ranks.  Inputs (49.6 GB at config 5)
+are far larger than L2 (126 MB), so no L2 flush is needed between steps.
+"""
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAK_FP64_DERIVED = 148 * 64 * 2 * 1.965e9      # DFMA/clk/SM x 2 flop x SMs x max clock
+
+
+def alg_flops(p, q, ne):
+    """plain 3-stage sum factorisation fwd+transpose, 3 comps, + 120 flop/qp."""
+    n = p + 1
+    return ne * (12 * (2 * q * n ** 3 + 3 * q * q * n * n + 3 * q ** 3 * n) + 120 * q ** 3)
+
+
+def alg_bytes(ndof, ne, q, per_elem):
+    """x read + y write + 9 qdata doubles per point (+ r_e per element)."""
+    return 16 * ndof + 72 * q ** 3 * ne + (8 * ne if per_elem else 0)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------------------ clocks
+
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, device_index, period=0.05):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period, self._stop = period, threading.Event()
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.h = None
+
+    def _reasons(self):
+        nv = self.nv
+        for fn in ("nvmlDeviceGetCurrentClocksEventReasons", "nvmlDeviceGetCurrentClocksThrottleReasons"):
+            if hasattr(nv, fn):
+                return getattr(nv, fn)(self.h)
+        return 0
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self._reasons()
+                for bit, name in REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self.h is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.h is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------ CPU oracle
+
+def oracle_sample_problem(P, bx, by, bz):
+    """A bx x by x bz brick of elements (corner at the origin) carved out of workload P."""
+    import synth
+    p = P.p
+    V = P.vertex_array()[:bz + 1, :by + 1, :bx + 1]
+    lam, mu = P.material_arrays()
+    lam, mu = lam[:bz, :by, :bx], mu[:bz, :by, :bx]
+    Nx, Ny, Nz = P.node_dims
+    x = P.x_slab(0, bz * p) if P.x is None else P.x
+    x = x.reshape(3, -1, Ny, Nx)[:, :bz * p + 1, :by * p + 1, :bx * p + 1]
+    Q = synth.Problem(P.name + "_brick", bx, by, bz, p, P.q, 1.0, 1.0, 1.0, V, lam, mu,
+                      np.ascontiguousarray(x).reshape(-1), 0, P.seed)
+    return Q
+
+
+def oracle_time(P, nelem):
+    """Run the oracle (as it stands) on a brick of ~nelem elements; return (seconds, elements)."""
+    import oracle
+    bx = min(P.nx, max(1, int(round(nelem ** (1 / 3)))))
+    by = min(P.ny, max(1, int(round((nelem / bx) ** 0.5))))
+    bz = min(P.nz, max(1, nelem // (bx * by)))
+    Q = oracle_sample_problem(P, bx, by, bz)
+    lam, mu = Q.material_arrays()
+    m = oracle.Mesh(Q.vertices, Q.p, Q.q, lam, mu, 0)
+    elems = [(ex, ey, ez) for ez in range(bz) for ey in range(by) for ex in range(bx)]
+    t = time.perf_counter()
+    oracle.apply_elements(m, Q.x, elems)
+    return time.perf_counter() - t, len(elems), f"{bx}x{by}x{bz} element brick of {P.name}"
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n:
+            return int(max(n))
+    except Exception:
+        pass
+    return os.cpu_count()
+
+
+def cpu_baseline(P, budget_s=12.0):
+    nel = 4
+    t, ne, desc = oracle_time(P, nel)
+    while t < budget_s / 4 and ne < P.num_elements:
+        nel = int(ne * max(2.0, min(8.0, budget_s / max(t, 1e-3) / 2)))
+        t, ne, desc = oracle_time(P, nel)
+    value = P.num_dofs * (ne / P.num_elements) / t / 1e9
+    return {"value": value, "unit": "GDoF/s", "cores": blas_threads(), "kind": "oracle",
+            "sample": f"{desc} ({ne} elements, {t:.1f} s; extrapolated to {P.num_elements} elements)"}
+
+
+# ------------------------------------------------------------------------------ helpers
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return ws, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def make_workload(cfg, p):
+    import synth
+    return synth.make_config(cfg, p, draw_x=False)
+
+
+def workload_desc(P):
+    geo = "perturbed" if P.vertices is not None else "affine"
+    mat = "LogNormal(0,0.5) per element" if P.per_element_material else f"lam={float(P.lam)}, mu={float(P.mu)}"
+    return (f"{P.name}: {P.nx}x{P.ny}x{P.nz} hexes, Q{P.p} q={P.q}, {geo} trilinear, {mat}, "
+            f"faces={P.dirichlet_faces}, {P.num_dofs} DoF")
+
+
+def reduce_max(val, ws):
+    if ws == 1:
+        return val
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([val], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------------------ sweep
+
+def sweep_config4(reps=10, warmup=3):
+    import torch
+    import synth
+    from paper_2601_08374_b200.elas import Operator, elas_profile, elas_profile_read
+    out = {}
+    for p in range(1, 9):
+        P = synth.make_config(4, p)
+        op = Operator.from_problem(P)
+        x = torch.from_numpy(P.x).cuda()
+        y = torch.empty_like(x)
+        for _ in range(warmup):
+            op.apply(x, y)
+        torch.cuda.synchronize()
+        elas_profile(op.h, True)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            op.apply(x, y)
+        b.record()
+        torch.cuda.synchronize()
+        kms, nl = elas_profile_read(op.h)
+        elas_profile(op.h, False)
+        t = a.elapsed_time(b) / reps / 1e3
+        tk = kms / nl / 1e3
+        F = alg_flops(p, P.q, P.num_elements)
+        B = alg_bytes(P.num_dofs, P.num_elements, P.q, False)
+        roof_t = max(F / PEAK_FP64_DERIVED, B / 8e12)
+        out[str(p)] = {"q": P.q, "dofs": P.num_dofs, "elements": P.num_elements,
+                       "gdofs": round(P.num_dofs / t / 1e9, 3), "ms_per_apply": round(t * 1e3, 4),
+                       "kernel_ms": round(tk * 1e3, 4),
+                       "fp64_tflops_alg": round(F / tk / 1e12, 2),
+                       "roofline_frac": round(roof_t / t, 4),
+                       "bound": "fp64" if F / PEAK_FP64_DERIVED > B / 8e12 else "hbm"}
+        op.close()
+        del x, y
+        torch.cuda.empty_cache()
+    return out
+
+
+# ------------------------------------------------------------------------------ arms
+
+def run_ours(args):
+    import torch
+    ws, rank, lrank = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(lrank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
+    else:
+        torch.cuda.set_device(0)
+    from paper_2601_08374_b200 import elas
+    from paper_2601_08374_b200.elas import Operator
+
+    P = make_workload(args.config, args.p)
+    b, e = elas.elas_slab_range(P.nz, rank, ws)
+    K0, K1 = b * P.p, e * P.p
+    t_gen = time.perf_counter()
+    x_np = P.x_slab(K0, K1)
+    t_gen = time.perf_counter() - t_gen
+    nccl_id = None
+    if ws > 1:
+        import torch.distributed as dist
+        obj = [elas.elas_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    stream = torch.cuda.current_stream()
+    t0 = time.perf_counter()
+    op = Operator.from_problem(P, rank=rank, nranks=ws, nccl_id=nccl_id, stream=stream)
+    setup_s = time.perf_counter() - t0
+    assert op.local_dofs == x_np.size
+    x_pin = torch.from_numpy(x_np).pin_memory()
+    del x_np
+    x = x_pin.cuda()
+    y = torch.empty_like(x)
+
+    for _ in range(args.warmup):
+        op.apply(x, y)
+    torch.cuda.synchronize()
+    barrier(ws)
+    elas.elas_profile(op.h, True)
+    elas.elas_profile_read(op.h)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        barrier(ws)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            op.apply(x, y)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+    elas.elas_profile(op.h, False)
+    kern_ms, nlaunch = elas.elas_profile_read(op.h)
+    t_ms = reduce_max(ev0.elapsed_time(ev1), ws)
+    kern_ms_per_apply = reduce_max(kern_ms / args.steps, ws)
+    ms_per_step = t_ms / args.steps
+    value = P.num_dofs / (ms_per_step / 1e3) / 1e9
+
+    # end to end through the C ABI with pinned HOST buffers (H2D + apply + D2H each step)
+    y_pin = torch.empty_like(x_pin).pin_memory()
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    op.apply_host(x_pin, y_pin)
+    barrier(ws)
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        op.apply_host(x_pin, y_pin)
+    t_e2e = reduce_max(time.perf_counter() - t, ws)
+    e2e_value = P.num_dofs / (t_e2e / e2e_steps) / 1e9
+    launches = op.launches_per_apply * args.steps
+
+    # roofline of the dominant kernel (the fused apply): algorithmic flops of this rank per apply
+    ne_local = P.nx * P.ny * (e - b)
+    F = alg_flops(P.p, P.q, ne_local)
+    B = alg_bytes(op.local_dofs, ne_local, P.q, P.per_element_material)
+    tk = kern_ms_per_apply / 1e3
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs")
+    roof = {"bound": "alu", "achieved": round(F / tk / 1e12, 3), "peak": round(PEAK_FP64_DERIVED / 1e12, 2),
+            "unit": "TFLOP/s", "frac": round(F / tk / PEAK_FP64_DERIVED, 4), "traffic": None,
+            "peak_kind": "derived FP64 DFMA pipe: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md 6)",
+            "alg_flops_per_apply": F, "alg_bytes_per_apply": B,
+            "hbm_achieved_gbs": round(B / tk / 1e9, 1),
+            "hbm_frac_of_measured": round(B / tk / 1e9 / hbm_peak, 4) if hbm_peak else None,
+            "kernel_share_of_step": round(kern_ms_per_apply / ms_per_step, 4),
+            "roofline_frac_step_8tbs": round(max(F / PEAK_FP64_DERIVED, B / 8e12) * ws / (ms_per_step / 1e3), 4)}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(f"cfg{args.config}" + (f"_p{args.p}" if args.config == 4 else ""))
+            if tr and ws == 1:
+                roof["traffic"] = tr.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    line = {"metric": "elasticity operator apply GDoF/s (FP64); % of FP64/HBM roofline",
+            "value": round(value, 4), "unit": "GDoF/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(P), "dofs": P.num_dofs, "elements": P.num_elements,
+                       "p": P.p, "q": P.q, "parallelism": f"z-slabs x{ws}" + (" (NCCL interface sum)" if ws > 1 else ""),
+                       "l2": "inputs larger than L2 (no flush needed)"},
+            "clocks": clk.summary(),
+            "e2e": {"value": round(e2e_value, 4), "unit": "GDoF/s", "steps": e2e_steps,
+                    "h2d_bytes_per_step": 8 * op.local_dofs * ws, "d2h_bytes_per_step": 8 * op.local_dofs * ws,
+                    "note": "elas_apply_host: pinned host x -> device, apply, device -> pinned host y"},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "setup_s": round(setup_s, 3), "x_generation_s": round(t_gen, 2)}
+    op.close()
+    del x, y
+    torch.cuda.empty_cache()
+    if ws == 1 and rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(P)
+    if ws == 1 and not args.no_sweep:
+        line["sweep"] = {"workload": "config 4: m^3 unit cube, m = round(255.44/p), q=p+2, affine, lam=1, mu=0.5, seed 3",
+                         "per_p": sweep_config4()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """The CPU oracle as it stands, on bounded samples of the same workload (rank 0 only)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    P = make_workload(args.config, args.p)
+    per_step = max(1, args.ref_elems if args.ref_elems else (16 if P.p >= 6 else 64))
+    for _ in range(args.warmup):
+        oracle_time(P, per_step)
+    ts, ne, desc = 0.0, 0, ""
+    for _ in range(args.steps):
+        t, n, desc = oracle_time(P, per_step)
+        ts += t
+        ne += n
+    sec_per_step = ts / args.steps
+    value = P.num_dofs * (ne / args.steps / P.num_elements) / sec_per_step / 1e9
+    line = {"metric": "elasticity operator apply GDoF/s (FP64); % of FP64/HBM roofline",
+            "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sec_per_step * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_desc(P), "dofs": P.num_dofs, "elements": P.num_elements,
+                       "p": P.p, "q": P.q},
+            "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": blas_threads(), "kind": "oracle",
+                             "sample": f"each step: {desc}, extrapolated to {P.num_elements} elements"},
+            "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=5, choices=[2, 3, 4, 5])
+    ap.add_argument("--p", type=int, default=6, help="degree for --config 4")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-elems", type=int, default=0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    ws, _, _ = dist_env()
+    if ws != args.gpus:
+        if not (ws == 1 and args.gpus == 1):
+            print(f"warning: --gpus {args.gpus} but WORLD_SIZE={ws}; using WORLD_SIZE", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,155 @@
+/*
+ * elas.h -- C ABI of libelas.so: the matrix-free (partial-assembly) action y = A x of the
+ * 3D linear-elasticity stiffness operator on tensor-product Q_p hexahedra, FP64, on B200.
+ *
+ * What the operator is (citations are to the paper text, /root/reference/PAPER.md):
+ *   - Hooke's law sigma = lambda (div u) I + 2 mu eps(u)                  PAPER.md:147-150, Eq. 3
+ *   - bilinear form a(u,v) = int sigma(u) : grad v                         PAPER.md:152-156, Eq. 4
+ *   - A_ij = a(phi_i, phi_j) (Galerkin system A U = F)                     PAPER.md:158-162, Eq. 5
+ *   - A = P^T G^T B^T D B G P applied on the fly (partial assembly)
+ *   - tensor-product basis + sum factorisation, O(p^4) per element
+ *   - one element-centric fused pass (macro-kernel fusion, Alg. 2)
+ *   - Voigt-symmetric stress at the quadrature points (Sec. 4.3, Eq. 6)
+ * Discretisation readings (where the paper is silent) are listed in DESIGN.md section 3:
+ * Lagrange basis on Gauss-Lobatto-Legendre nodes, q-point Gauss-Legendre quadrature per
+ * direction, trilinear geometry, reference cube [0,1]^3.
+ *
+ * Mesh and vector conventions (R6):
+ *   - structured nx x ny x nz grid of trilinear hexahedra, vertex (i,j,k) at
+ *     vertices[((k*(ny+1) + j)*(nx+1) + i)*3 + {0,1,2}]  (x fastest);
+ *   - global node (I,J,K), I in [0, nx p], id = I + Nx (J + Ny K), Nx = nx p + 1, ...;
+ *   - vectors are component-blocked: dof = c N + id, c = 0,1,2 (all x, then y, then z).
+ *
+ * Multi-GPU (one process per GPU): the element grid is split into contiguous z-slabs,
+ * rank r owning element layers ez in [floor(r nz / P), floor((r+1) nz / P)).  Rank r holds
+ * node planes K in [ez_begin p, ez_end p] (both ends): interface planes are replicated and,
+ * after elas_apply, both replicas hold the full sum (the P^T of PAPER.md:169).
+ *
+ * Error behaviour: functions return ELAS_OK (0) or a negative ELAS_E* code; elas_create
+ * returns NULL.  In every failing case elas_last_error() returns a thread-local message.
+ * Asynchronous CUDA faults surface at the next call that synchronises.
+ */
+#ifndef ELAS_H
+#define ELAS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ELAS_OK 0
+#define ELAS_EINVAL (-1) /* bad sizes, p not in [1,8], q not in {p+1,p+2}, NULL or misaligned
+                            pointers, x == y, mu <= 0 or 3 lambda + 2 mu <= 0, or a call
+                            that does not match the op's mode                        */
+#define ELAS_EGEOM (-2)  /* det J <= 0 at some quadrature point                         */
+#define ELAS_ENOMEM (-3) /* device or host allocation failed                            */
+#define ELAS_ECUDA (-4)  /* CUDA runtime error (message has the CUDA error string)       */
+#define ELAS_ENCCL (-5)  /* NCCL error (multi-GPU exchange)                             */
+
+/* Dirichlet face bits: all three components of every node on the face are constrained. */
+#define ELAS_FACE_XMIN 1u
+#define ELAS_FACE_XMAX 2u
+#define ELAS_FACE_YMIN 4u
+#define ELAS_FACE_YMAX 8u
+#define ELAS_FACE_ZMIN 16u
+#define ELAS_FACE_ZMAX 32u
+
+typedef struct elas_op elas_op; /* opaque; owned by the library */
+
+typedef struct {
+  int32_t nx, ny, nz;           /* GLOBAL elements per axis, each >= 1                      */
+  const double* vertices;       /* HOST, (nz+1)(ny+1)(nx+1)*3 doubles, x fastest, xyz per
+                                   vertex; NULL => uniform grid on [0,lx]x[0,ly]x[0,lz]      */
+  double lx, ly, lz;            /* > 0; used only when vertices == NULL                     */
+  uint32_t dirichlet_faces;     /* OR of ELAS_FACE_* ; y = Z A Z x + (I - Z) x               */
+  int32_t material_per_element; /* 0: lambda, mu point to 1 value each;
+                                   1: to nx*ny*nz values each (element order x fastest)     */
+  const void* nccl_id;          /* NULL, or a HOST pointer to a 128-byte ncclUniqueId shared
+                                   by all ranks: the library then owns an NCCL communicator
+                                   and does the interface sum inside elas_apply             */
+  int32_t rank, nranks;         /* nranks == 1: single GPU.  nranks > 1 and nccl_id == NULL:
+                                   "external exchange" mode -- elas_apply leaves the
+                                   interface planes as LOCAL partial sums and the caller
+                                   completes them with elas_interface_add                   */
+} elas_mesh;
+
+/* Build the operator on the current CUDA device: validates the inputs, builds the 1D
+ * tables (GLL nodes, Gauss-Legendre rule, Lagrange values/derivatives; host), copies the
+ * vertices of this rank's slab to the device and runs the quadrature-data setup kernel
+ * (J, det J, A = J^{-1}, W = w det J; stores A~ = sqrt(mu_e W) A per point and
+ * r_e = lambda_e / mu_e per element).  Synchronises.  lambda/mu: HOST pointers.
+ * q must be p+1 or p+2.  Host arrays are copied; the caller may free them on return.
+ * Returns NULL on error (see elas_last_error). */
+elas_op* elas_create(const elas_mesh* mesh, int p, int q, const double* lambda, const double* mu);
+
+/* y = A x (overwrite), or y = Z A Z x + (I - Z) x with Dirichlet faces.
+ * x, y: DEVICE pointers on the op's device, elas_local_dofs(op) doubles each, component-
+ * blocked over this rank's node planes, 8-byte aligned, not aliased.  Asynchronous on the
+ * op's stream (see elas_set_stream).  A distributed op owns halo buffers: serialise its
+ * applies.  Returns ELAS_OK or ELAS_EINVAL / ELAS_ECUDA / ELAS_ENCCL. */
+int elas_apply(elas_op* op, const double* x, double* y);
+
+/* End-to-end form of elas_apply: x_host, y_host are HOST pointers (pinned recommended);
+ * copies x to an op-owned device buffer, applies, copies y back, and synchronises the
+ * op's stream.  Returns as elas_apply (ELAS_ENOMEM if the staging buffers fail). */
+int elas_apply_host(elas_op* op, const double* x_host, double* y_host);
+
+/* External-exchange mode only (nranks > 1, nccl_id == NULL): add the neighbours' partial
+ * interface planes into y on the op's stream.  lo_halo: the partial plane of rank r-1 for
+ * the plane K = ez_begin p (NULL on rank 0); hi_halo: the partial plane of rank r+1 for
+ * K = ez_end p (NULL on the last rank).  Each is 3 * Nx * Ny doubles, component-blocked,
+ * DEVICE pointers.  Constrained (Dirichlet) rows are left untouched.  Returns ELAS_OK,
+ * ELAS_EINVAL or ELAS_ECUDA. */
+int elas_interface_add(elas_op* op, double* y, const double* lo_halo, const double* hi_halo);
+
+/* Release everything the op owns (device memory, communicator, streams).  NULL-safe. */
+void elas_destroy(elas_op* op);
+
+/* Length of x and y on this rank: 3 * Nx * Ny * (nz_local p + 1).  -1 if op == NULL. */
+int64_t elas_local_dofs(const elas_op* op);
+
+/* This rank's element-layer range [ez_begin, ez_end).  ELAS_OK or ELAS_EINVAL. */
+int elas_local_zrange(const elas_op* op, int32_t* ez_begin, int32_t* ez_end);
+
+/* Make subsequent applies run on `cuda_stream` (a cudaStream_t; NULL = legacy default). */
+int elas_set_stream(elas_op* op, void* cuda_stream);
+
+/* Number of kernel launches one elas_apply issues (for the bench's launch accounting). */
+int elas_launches_per_apply(const elas_op* op);
+
+/* Measurement hook (used by bench.py): while enabled, every launch of the fused apply
+ * kernel inside elas_apply is bracketed by CUDA events on the op's stream.
+ * elas_profile_read synchronises on the last event, returns the summed kernel time (ms) and
+ * the number of bracketed launches since the previous read, and resets the counters.
+ * Both return ELAS_OK, ELAS_EINVAL or ELAS_ECUDA. */
+int elas_profile(elas_op* op, int enable);
+int elas_profile_read(elas_op* op, double* apply_kernel_ms, int64_t* launches);
+
+/* Thread-local message describing the last error on this thread ("" if none). */
+const char* elas_last_error(void);
+
+/* Host-only helpers (no GPU needed) -------------------------------------------------- */
+
+/* The slab partition: [floor(rank nz / nranks), floor((rank+1) nz / nranks)).
+ * ELAS_EINVAL if nz < nranks, nranks < 1 or rank outside [0, nranks). */
+int elas_slab_range(int32_t nz, int32_t rank, int32_t nranks, int32_t* ez_begin, int32_t* ez_end);
+
+/* The 1D tables the kernels use, for inspection: nodes[p+1] (GLL on [0,1]), points[q],
+ * weights[q] (Gauss-Legendre on [0,1], sum 1), B[q*(p+1)] and D[q*(p+1)] with
+ * B[a*(p+1)+i] = l_i(g_a), D[a*(p+1)+i] = l_i'(g_a).  Any output may be NULL.
+ * ELAS_OK or ELAS_EINVAL (p not in [1,8], q not in [1,16]). */
+int elas_tables(int p, int q, double* nodes, double* points, double* weights, double* B, double* D);
+
+/* Create a fresh 128-byte ncclUniqueId into `id_out` (host memory) on ONE rank; broadcast it
+ * to the others (e.g. over a torch.distributed group) and pass it as elas_mesh.nccl_id.
+ * ELAS_OK, ELAS_EINVAL (NULL) or ELAS_ENCCL. */
+int elas_nccl_unique_id(void* id_out);
+
+/* Library version (major*10000 + minor*100 + patch). */
+int elas_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ELAS_H */

@@ -31,6 +31,7 @@ from .elasticity import (  # noqa: F401
     Mesh,
     element_stiffness,
     apply,
+    apply_elements,
     apply_rows,
     assemble_dense,
     constrained_mask,

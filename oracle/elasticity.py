@@ -137,25 +137,21 @@ def element_stiffness(X, lam, mu, tables, rows=None):
     J, detJ, W = element_geometry(X, g, w3)
     A = np.linalg.inv(J)                                   # A = J^{-1}, (q^3, 3, 3)
     # physical gradients Phi[m][l, qp] = sum_k Gref[k][l, qp] A[qp, k, m]
-    Phi = np.einsum("klq,qkm->mlq", Gref, A)
+    Phi = np.einsum("klq,qkm->mlq", Gref, A, optimize=True)
     if rows is None:
         rows = np.arange(3 * nn)
     rows = np.asarray(rows)
     comp, node = rows // nn, rows % nn
     # M[k][l][r, J] = sum_qp W Phi_k[node_r, qp] Phi_l[J, qp]
     PW = Phi[:, node, :] * W                               # (3, R, q^3)
-    M = np.einsum("krq,lJq->klrJ", PW, Phi)                # (3, 3, R, n^3)
-    trace = M[0, 0] + M[1, 1] + M[2, 2]
+    M = np.einsum("krq,lJq->klrJ", PW, Phi, optimize=True)  # (3, 3, R, n^3)
+    trace = M[0, 0] + M[1, 1] + M[2, 2]                    # (R, n^3)
     R = rows.size
-    K = np.zeros((R, 3 * nn))
-    for r in range(R):
-        i = comp[r]
-        for j in range(3):
-            blk = lam * M[i, j, r] + mu * M[j, i, r]
-            if i == j:
-                blk = blk + mu * trace[r]
-            K[r, j * nn:(j + 1) * nn] = blk
-    return K
+    r = np.arange(R)
+    # row r = (i, I) with i = comp[r]; block j: lam M[i, j, r] + mu M[j, i, r] (+ mu tr if i == j)
+    K = lam * M[comp, :, r, :] + mu * M[:, comp, r, :].transpose(1, 0, 2)   # (R, 3, n^3)
+    K[r, comp, :] += mu * trace
+    return K.reshape(R, 3 * nn)
 
 
 # ----------------------------------------------------------------------------------------
@@ -198,19 +194,24 @@ def _elements(mesh):
 def apply(mesh, x):
     """y = Z A Z x + (I - Z) x, element by element (full mode)."""
     x = np.asarray(x, dtype=np.float64).reshape(-1)
-    N = mesh.num_nodes
-    assert x.size == 3 * N
+    assert x.size == mesh.num_dofs
     Z = constrained_mask(mesh)
-    xz = np.where(Z, 0.0, x)
+    y = apply_elements(mesh, np.where(Z, 0.0, x), _elements(mesh))
+    y[Z] = x[Z]
+    return y
+
+
+def apply_elements(mesh, xz, elements):
+    """sum_e G_e^T K_e G_e xz over the given elements (x already masked); the loop of apply."""
+    N = mesh.num_nodes
     tables = reference_tables(mesh.p, mesh.q)
     y = np.zeros(3 * N)
-    for ex, ey, ez in _elements(mesh):
+    for ex, ey, ez in elements:
         nodes = element_nodes(mesh, ex, ey, ez)
         dofs = np.concatenate([c * N + nodes for c in range(3)])
         K = element_stiffness(element_vertices(mesh, ex, ey, ez),
                               mesh.lam[ez, ey, ex], mesh.mu[ez, ey, ex], tables)
         np.add.at(y, dofs, K @ xz[dofs])
-    y[Z] = x[Z]
     return y
 
 

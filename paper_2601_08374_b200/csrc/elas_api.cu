@@ -1,0 +1,465 @@
+// The C ABI of libelas.so (include/elas.h): operator construction, apply, multi-GPU slab
+// exchange over NCCL, and host-only helpers.
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "elas_internal.h"
+
+#define ELAS_VERSION 10000
+
+namespace elas {
+
+namespace {
+thread_local std::string g_err;
+
+// per-degree dispatch (defined by ELAS_DEFINE_DEGREE in elas_apply_p<P>.cu)
+}  // namespace
+
+#define DECL(P)                                                                                  \
+  cudaError_t apply_info_p##P(int q, ApplyLaunch* info);                                         \
+  cudaError_t apply_launch_p##P(int q, const Slab& s, const double* x, double* y, const double* qd, \
+                                const double* rr, const double* tables, int64_t e_begin,        \
+                                int64_t e_end, cudaStream_t st);
+DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
+#undef DECL
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+cudaError_t apply_info(int p, int q, ApplyLaunch* info) {
+  switch (p) {
+    case 1: return apply_info_p1(q, info);
+    case 2: return apply_info_p2(q, info);
+    case 3: return apply_info_p3(q, info);
+    case 4: return apply_info_p4(q, info);
+    case 5: return apply_info_p5(q, info);
+    case 6: return apply_info_p6(q, info);
+    case 7: return apply_info_p7(q, info);
+    case 8: return apply_info_p8(q, info);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t apply_launch(int p, int q, const Slab& s, const double* x, double* y, const double* qd,
+                         const double* rr, const double* tables, int64_t e_begin, int64_t e_end,
+                         cudaStream_t st) {
+  switch (p) {
+#define CASE(P) case P: return apply_launch_p##P(q, s, x, y, qd, rr, tables, e_begin, e_end, st);
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace elas
+
+using elas::Slab;
+using elas::set_error;
+
+struct elas_op {
+  int p = 0, q = 0, rank = 0, nranks = 1;
+  int32_t ez0 = 0, ez1 = 0;
+  Slab slab{};
+  int device = 0;
+  bool external = false;            // nranks > 1 without a communicator
+  double* qd = nullptr;             // 9 q^3 doubles per element
+  double* rr = nullptr;             // lambda/mu per element
+  double* tab = nullptr;            // B then D (q x (p+1) each)
+  double* xs = nullptr;             // staging for elas_apply_host
+  double* ys = nullptr;
+  cudaStream_t stream = nullptr;
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_boundary = nullptr, ev_comm = nullptr;
+  double* halo_lo = nullptr;
+  double* halo_hi = nullptr;
+  // measurement hook
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;   // pairs (start, stop), reused
+  size_t prof_used = 0;
+};
+
+namespace {
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? ELAS_ENOMEM : ELAS_ECUDA;
+}
+
+int nccl_fail(ncclResult_t r, const char* what) {
+  set_error(std::string(what) + ": " + ncclGetErrorString(r));
+  return ELAS_ENCCL;
+}
+
+#define CUDA_OR(expr, what)                   \
+  do {                                        \
+    cudaError_t e_ = (expr);                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+#define NCCL_OR(expr, what)                   \
+  do {                                        \
+    ncclResult_t r_ = (expr);                 \
+    if (r_ != ncclSuccess) return nccl_fail(r_, what); \
+  } while (0)
+
+void free_op(elas_op* op) {
+  if (!op) return;
+  cudaFree(op->qd);
+  cudaFree(op->rr);
+  cudaFree(op->tab);
+  cudaFree(op->xs);
+  cudaFree(op->ys);
+  cudaFree(op->halo_lo);
+  cudaFree(op->halo_hi);
+  if (op->comm) ncclCommDestroy(op->comm);
+  if (op->comm_stream) cudaStreamDestroy(op->comm_stream);
+  if (op->ev_boundary) cudaEventDestroy(op->ev_boundary);
+  if (op->ev_comm) cudaEventDestroy(op->ev_comm);
+  for (cudaEvent_t ev : op->prof_ev) cudaEventDestroy(ev);
+  delete op;
+}
+
+int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* mu) {
+  const int p = op->p, q = op->q;
+  const int nx = m->nx, ny = m->ny;
+  const int nzl = op->ez1 - op->ez0;
+  Slab& s = op->slab;
+  s.nx = nx;
+  s.ny = ny;
+  s.nz = nzl;
+  s.Nx = nx * p + 1;
+  s.Ny = ny * p + 1;
+  s.Nz = nzl * p + 1;
+  s.nodes = (int64_t)s.Nx * s.Ny * s.Nz;
+  uint32_t f = m->dirichlet_faces & 15u;
+  if ((m->dirichlet_faces & ELAS_FACE_ZMIN) && op->rank == 0) f |= ELAS_FACE_ZMIN;
+  if ((m->dirichlet_faces & ELAS_FACE_ZMAX) && op->rank == op->nranks - 1) f |= ELAS_FACE_ZMAX;
+  s.faces = f;
+
+  const int64_t ne = (int64_t)nx * ny * nzl;
+  // vertices of the slab (planes ez0 .. ez1)
+  const int64_t vplane = (int64_t)(nx + 1) * (ny + 1);
+  std::vector<double> V((size_t)(vplane * (nzl + 1) * 3));
+  for (int k = 0; k <= nzl; ++k)
+    for (int j = 0; j <= ny; ++j)
+      for (int i = 0; i <= nx; ++i) {
+        const int64_t lv = ((int64_t)k * (ny + 1) + j) * (nx + 1) + i;
+        const int64_t gv = ((int64_t)(k + op->ez0) * (ny + 1) + j) * (nx + 1) + i;
+        for (int c = 0; c < 3; ++c) {
+          double val;
+          if (m->vertices) {
+            val = m->vertices[gv * 3 + c];
+          } else {
+            const double L = c == 0 ? m->lx : (c == 1 ? m->ly : m->lz);
+            const int n = c == 0 ? m->nx : (c == 1 ? m->ny : m->nz);
+            const int idx = c == 0 ? i : (c == 1 ? j : k + op->ez0);
+            val = (idx == n) ? L : idx * (L / n);
+          }
+          V[lv * 3 + c] = val;
+        }
+      }
+  // material of the slab
+  std::vector<double> lam((size_t)ne), muv((size_t)ne);
+  const int64_t off = (int64_t)op->ez0 * nx * ny;
+  for (int64_t e = 0; e < ne; ++e) {
+    lam[e] = m->material_per_element ? lambda[off + e] : lambda[0];
+    muv[e] = m->material_per_element ? mu[off + e] : mu[0];
+    if (!(muv[e] > 0.0) || !(3.0 * lam[e] + 2.0 * muv[e] > 0.0) || !std::isfinite(lam[e])) {
+      set_error("invalid material: need mu > 0 and 3 lambda + 2 mu > 0 (element " +
+                std::to_string(off + e) + ")");
+      return ELAS_EINVAL;
+    }
+  }
+  // 1D tables
+  const int n = p + 1;
+  std::vector<double> g(q), w(q), tabh(2 * q * n);
+  elas::host_tables(p, q, nullptr, g.data(), w.data(), tabh.data(), tabh.data() + q * n);
+
+  double *dV = nullptr, *dlam = nullptr, *dmu = nullptr;
+  int* dbad = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(dV);
+    cudaFree(dlam);
+    cudaFree(dmu);
+    cudaFree(dbad);
+  };
+  cudaError_t e;
+  const size_t qbytes = sizeof(double) * 9 * (size_t)q * q * q * (size_t)ne;
+  if ((e = cudaMalloc(&op->qd, qbytes)) != cudaSuccess ||
+      (e = cudaMalloc(&op->rr, sizeof(double) * ne)) != cudaSuccess ||
+      (e = cudaMalloc(&op->tab, sizeof(double) * tabh.size())) != cudaSuccess ||
+      (e = cudaMalloc(&dV, sizeof(double) * V.size())) != cudaSuccess ||
+      (e = cudaMalloc(&dlam, sizeof(double) * ne)) != cudaSuccess ||
+      (e = cudaMalloc(&dmu, sizeof(double) * ne)) != cudaSuccess ||
+      (e = cudaMalloc(&dbad, sizeof(int))) != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "cudaMalloc (operator setup)");
+  }
+  int rc = ELAS_OK;
+  do {
+    if ((e = cudaMemcpy(op->tab, tabh.data(), sizeof(double) * tabh.size(), cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(dV, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(dlam, lam.data(), sizeof(double) * ne, cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(dmu, muv.data(), sizeof(double) * ne, cudaMemcpyHostToDevice)) ||
+        (e = cudaMemset(dbad, 0, sizeof(int)))) {
+      rc = cuda_fail(e, "cudaMemcpy (operator setup)");
+      break;
+    }
+    if ((e = elas::launch_qdata(p, q, s, dV, dlam, dmu, g.data(), w.data(), op->qd, op->rr, dbad, op->stream)) ||
+        (e = cudaStreamSynchronize(op->stream))) {
+      rc = cuda_fail(e, "qdata setup kernel");
+      break;
+    }
+    int bad = 0;
+    if ((e = cudaMemcpy(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost))) {
+      rc = cuda_fail(e, "cudaMemcpy");
+      break;
+    }
+    if (bad) {
+      set_error("det J <= 0 at some quadrature point (inverted or degenerate element)");
+      rc = ELAS_EGEOM;
+    }
+  } while (0);
+  cleanup();
+  return rc;
+}
+
+int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1, cudaStream_t st) {
+  if (e1 <= e0) return ELAS_OK;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (op->prof) {
+    while (op->prof_ev.size() < op->prof_used + 2) {
+      cudaEvent_t ev;
+      CUDA_OR(cudaEventCreate(&ev), "cudaEventCreate");
+      op->prof_ev.push_back(ev);
+    }
+    ev0 = op->prof_ev[op->prof_used];
+    ev1 = op->prof_ev[op->prof_used + 1];
+    op->prof_used += 2;
+    CUDA_OR(cudaEventRecord(ev0, st), "cudaEventRecord");
+  }
+  cudaError_t e = elas::apply_launch(op->p, op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st);
+  if (e != cudaSuccess) return cuda_fail(e, "apply kernel launch");
+  if (op->prof) CUDA_OR(cudaEventRecord(ev1, st), "cudaEventRecord");
+  return ELAS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int elas_version(void) { return ELAS_VERSION; }
+
+int elas_nccl_unique_id(void* id_out) {
+  if (!id_out) { set_error("elas_nccl_unique_id: NULL output"); return ELAS_EINVAL; }
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  std::memcpy(id_out, &id, sizeof(id));
+  return ELAS_OK;
+}
+
+const char* elas_last_error(void) { return elas::g_err.c_str(); }
+
+int elas_slab_range(int32_t nz, int32_t rank, int32_t nranks, int32_t* ez_begin, int32_t* ez_end) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || nz < nranks) {
+    set_error("elas_slab_range: need 1 <= nranks <= nz and 0 <= rank < nranks");
+    return ELAS_EINVAL;
+  }
+  if (ez_begin) *ez_begin = (int32_t)(((int64_t)rank * nz) / nranks);
+  if (ez_end) *ez_end = (int32_t)(((int64_t)(rank + 1) * nz) / nranks);
+  return ELAS_OK;
+}
+
+int elas_tables(int p, int q, double* nodes, double* points, double* weights, double* B, double* D) {
+  int rc = elas::host_tables(p, q, nodes, points, weights, B, D);
+  if (rc) set_error("elas_tables: need 1 <= p <= 8 and 1 <= q <= 16");
+  return rc;
+}
+
+elas_op* elas_create(const elas_mesh* m, int p, int q, const double* lambda, const double* mu) {
+  elas::g_err.clear();
+  if (!m || !lambda || !mu) { set_error("elas_create: NULL mesh/lambda/mu"); return nullptr; }
+  if (p < 1 || p > 8) { set_error("elas_create: p must be in [1, 8]"); return nullptr; }
+  if (q != p + 1 && q != p + 2) { set_error("elas_create: q must be p+1 or p+2"); return nullptr; }
+  if (m->nx < 1 || m->ny < 1 || m->nz < 1) { set_error("elas_create: nx, ny, nz must be >= 1"); return nullptr; }
+  if (!m->vertices && !(m->lx > 0 && m->ly > 0 && m->lz > 0)) {
+    set_error("elas_create: lx, ly, lz must be > 0 when vertices == NULL");
+    return nullptr;
+  }
+  if (m->dirichlet_faces & ~63u) { set_error("elas_create: unknown Dirichlet face bits"); return nullptr; }
+  const int64_t Nx = (int64_t)m->nx * p + 1, Ny = (int64_t)m->ny * p + 1;
+  if (Nx * Ny * ((int64_t)m->nz * p + 1) * 3 >= (int64_t)1 << 31) {
+    // 32-bit node indices inside the kernels (I, J, K); vector offsets are 64-bit but we
+    // keep the global dof count below 2^31 as documented.
+    set_error("elas_create: more than 2^31 - 1 dofs per rank is not supported");
+    return nullptr;
+  }
+  elas_op* op = new elas_op();
+  op->p = p;
+  op->q = q;
+  op->nranks = m->nranks < 1 ? 1 : m->nranks;
+  op->rank = m->rank;
+  int32_t b, e;
+  if (elas_slab_range(m->nz, op->rank, op->nranks, &b, &e) != ELAS_OK) { free_op(op); return nullptr; }
+  op->ez0 = b;
+  op->ez1 = e;
+  cudaGetDevice(&op->device);
+  int rc = build(op, m, lambda, mu);
+  if (rc != ELAS_OK) { free_op(op); return nullptr; }
+  if (op->nranks > 1) {
+    const size_t pbytes = sizeof(double) * 3 * (size_t)op->slab.Nx * op->slab.Ny;
+    cudaError_t ce;
+    if ((ce = cudaMalloc(&op->halo_lo, pbytes)) || (ce = cudaMalloc(&op->halo_hi, pbytes))) {
+      cuda_fail(ce, "cudaMalloc (halo planes)");
+      free_op(op);
+      return nullptr;
+    }
+    if (m->nccl_id) {
+      ncclUniqueId id;
+      std::memcpy(&id, m->nccl_id, sizeof(id));
+      ncclResult_t r = ncclCommInitRank(&op->comm, op->nranks, id, op->rank);
+      if (r != ncclSuccess) { nccl_fail(r, "ncclCommInitRank"); op->comm = nullptr; free_op(op); return nullptr; }
+      if ((ce = cudaStreamCreateWithFlags(&op->comm_stream, cudaStreamNonBlocking)) ||
+          (ce = cudaEventCreateWithFlags(&op->ev_boundary, cudaEventDisableTiming)) ||
+          (ce = cudaEventCreateWithFlags(&op->ev_comm, cudaEventDisableTiming))) {
+        cuda_fail(ce, "stream/event creation");
+        free_op(op);
+        return nullptr;
+      }
+    } else {
+      op->external = true;
+    }
+  }
+  return op;
+}
+
+void elas_destroy(elas_op* op) {
+  if (op) cudaStreamSynchronize(op->stream);
+  free_op(op);
+}
+
+int64_t elas_local_dofs(const elas_op* op) { return op ? 3 * op->slab.nodes : -1; }
+
+int elas_local_zrange(const elas_op* op, int32_t* ez_begin, int32_t* ez_end) {
+  if (!op) { set_error("elas_local_zrange: NULL op"); return ELAS_EINVAL; }
+  if (ez_begin) *ez_begin = op->ez0;
+  if (ez_end) *ez_end = op->ez1;
+  return ELAS_OK;
+}
+
+int elas_set_stream(elas_op* op, void* st) {
+  if (!op) { set_error("elas_set_stream: NULL op"); return ELAS_EINVAL; }
+  op->stream = (cudaStream_t)st;
+  return ELAS_OK;
+}
+
+int elas_profile(elas_op* op, int enable) {
+  if (!op) { set_error("elas_profile: NULL op"); return ELAS_EINVAL; }
+  op->prof = enable != 0;
+  op->prof_used = 0;
+  return ELAS_OK;
+}
+
+int elas_profile_read(elas_op* op, double* ms, int64_t* launches) {
+  if (!op) { set_error("elas_profile_read: NULL op"); return ELAS_EINVAL; }
+  double total = 0.0;
+  if (op->prof_used) CUDA_OR(cudaEventSynchronize(op->prof_ev[op->prof_used - 1]), "cudaEventSynchronize");
+  for (size_t i = 0; i + 1 < op->prof_used; i += 2) {
+    float t = 0.f;
+    CUDA_OR(cudaEventElapsedTime(&t, op->prof_ev[i], op->prof_ev[i + 1]), "cudaEventElapsedTime");
+    total += t;
+  }
+  if (ms) *ms = total;
+  if (launches) *launches = (int64_t)(op->prof_used / 2);
+  op->prof_used = 0;
+  return ELAS_OK;
+}
+
+int elas_launches_per_apply(const elas_op* op) {
+  if (!op) return -1;
+  if (op->nranks == 1 || op->external) return 2;  // init + apply
+  const int nzl = op->ez1 - op->ez0;
+  const bool lo = op->rank > 0, hi = op->rank < op->nranks - 1;
+  int n = 1;                                       // init
+  if (lo && hi && nzl > 1) n += 2; else n += 1;    // boundary layer(s)
+  if (nzl - (int)lo - (int)hi > 0) n += 1;         // interior
+  n += (int)lo + (int)hi;                          // plane adds
+  return n;
+}
+
+int elas_apply(elas_op* op, const double* x, double* y) {
+  if (!op || !x || !y) { set_error("elas_apply: NULL argument"); return ELAS_EINVAL; }
+  if (x == y) { set_error("elas_apply: x and y must not alias"); return ELAS_EINVAL; }
+  if (((uintptr_t)x | (uintptr_t)y) & 7u) { set_error("elas_apply: x, y must be 8-byte aligned"); return ELAS_EINVAL; }
+  const Slab& s = op->slab;
+  cudaStream_t st = op->stream;
+  CUDA_OR(elas::launch_init(s, x, y, st), "init kernel launch");
+  const int64_t layer = (int64_t)s.nx * s.ny;
+  const int64_t ne = layer * s.nz;
+  if (op->nranks == 1 || op->external) return range_apply(op, x, y, 0, ne, st);
+
+  // NCCL slab mode: boundary layers, exchange overlapped with the interior, plane add.
+  const bool lo = op->rank > 0, hi = op->rank < op->nranks - 1;
+  int64_t int0 = 0, int1 = ne;
+  int rc;
+  if (lo) { if ((rc = range_apply(op, x, y, 0, layer, st))) return rc; int0 = layer; }
+  if (hi && ne - layer >= int0) { if ((rc = range_apply(op, x, y, ne - layer, ne, st))) return rc; int1 = ne - layer; }
+  else if (hi) int1 = int0;
+  CUDA_OR(cudaEventRecord(op->ev_boundary, st), "cudaEventRecord");
+  CUDA_OR(cudaStreamWaitEvent(op->comm_stream, op->ev_boundary, 0), "cudaStreamWaitEvent");
+  const int64_t plane = (int64_t)s.Nx * s.Ny;
+  NCCL_OR(ncclGroupStart(), "ncclGroupStart");
+  for (int c = 0; c < 3; ++c) {
+    if (lo) {
+      NCCL_OR(ncclSend(y + c * s.nodes, plane, ncclDouble, op->rank - 1, op->comm, op->comm_stream), "ncclSend");
+      NCCL_OR(ncclRecv(op->halo_lo + c * plane, plane, ncclDouble, op->rank - 1, op->comm, op->comm_stream), "ncclRecv");
+    }
+    if (hi) {
+      NCCL_OR(ncclSend(y + c * s.nodes + (int64_t)(s.Nz - 1) * plane, plane, ncclDouble, op->rank + 1, op->comm,
+                       op->comm_stream), "ncclSend");
+      NCCL_OR(ncclRecv(op->halo_hi + c * plane, plane, ncclDouble, op->rank + 1, op->comm, op->comm_stream), "ncclRecv");
+    }
+  }
+  NCCL_OR(ncclGroupEnd(), "ncclGroupEnd");
+  CUDA_OR(cudaEventRecord(op->ev_comm, op->comm_stream), "cudaEventRecord");
+  if ((rc = range_apply(op, x, y, int0, int1, st))) return rc;
+  CUDA_OR(cudaStreamWaitEvent(st, op->ev_comm, 0), "cudaStreamWaitEvent");
+  if (lo) CUDA_OR(elas::launch_plane_add(s, 0, y, op->halo_lo, st), "plane add launch");
+  if (hi) CUDA_OR(elas::launch_plane_add(s, s.Nz - 1, y, op->halo_hi, st), "plane add launch");
+  return ELAS_OK;
+}
+
+int elas_interface_add(elas_op* op, double* y, const double* lo_halo, const double* hi_halo) {
+  if (!op || !y) { set_error("elas_interface_add: NULL argument"); return ELAS_EINVAL; }
+  if (!op->external) { set_error("elas_interface_add: only for external-exchange ops (nranks > 1, nccl_id NULL)"); return ELAS_EINVAL; }
+  const bool lo = op->rank > 0, hi = op->rank < op->nranks - 1;
+  if ((lo_halo != nullptr) != lo || (hi_halo != nullptr) != hi) {
+    set_error("elas_interface_add: halo pointers do not match the rank's neighbours");
+    return ELAS_EINVAL;
+  }
+  if (lo) CUDA_OR(elas::launch_plane_add(op->slab, 0, y, lo_halo, op->stream), "plane add launch");
+  if (hi) CUDA_OR(elas::launch_plane_add(op->slab, op->slab.Nz - 1, y, hi_halo, op->stream), "plane add launch");
+  return ELAS_OK;
+}
+
+int elas_apply_host(elas_op* op, const double* xh, double* yh) {
+  if (!op || !xh || !yh) { set_error("elas_apply_host: NULL argument"); return ELAS_EINVAL; }
+  const size_t bytes = sizeof(double) * 3 * (size_t)op->slab.nodes;
+  if (!op->xs) CUDA_OR(cudaMalloc(&op->xs, bytes), "cudaMalloc (staging)");
+  if (!op->ys) CUDA_OR(cudaMalloc(&op->ys, bytes), "cudaMalloc (staging)");
+  CUDA_OR(cudaMemcpyAsync(op->xs, xh, bytes, cudaMemcpyHostToDevice, op->stream), "cudaMemcpyAsync H2D");
+  int rc = elas_apply(op, op->xs, op->ys);
+  if (rc) return rc;
+  CUDA_OR(cudaMemcpyAsync(yh, op->ys, bytes, cudaMemcpyDeviceToHost, op->stream), "cudaMemcpyAsync D2H");
+  CUDA_OR(cudaStreamSynchronize(op->stream), "cudaStreamSynchronize");
+  return ELAS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,422 @@
+// The fused sm_100a apply kernel: y += G^T B^T D B G x for a block of elements per CTA.
+//
+// One element-centric pass (macro-kernel fusion, Alg. 2): the E-vector
+// gather, the forward sum factorisation (three staged 1D contractions),
+// the pointwise Voigt-symmetric stress at every quadrature point, the
+// transposed contractions and the scatter-add all happen inside this kernel; intermediates
+// live in shared memory and registers only.  "Fibers to slices" becomes:
+// every stage is a set of independent 1D fibers, one thread per fiber and the three
+// displacement components blocked in registers, with shared-memory transposes between
+// stages laid out so that warp accesses are bank-conflict free.
+//
+// Stage order per CTA (EB elements, NT threads, 4 barriers):
+//   Z : gather x (zeroing Dirichlet dofs) along z-columns and contract in z with B and D
+//         u[c][k]            -> Zb[c][a3], Zd[c][a3]                       (registers -> smem sZ)
+//   Y : contract in y        -> Y0 = By Zb, Y1 = Dy Zb, Y2 = By Zd          (sZ -> sY)
+//   X : contract in x        -> G[c][d][a1] = d u_c / d xi_d at the q points of the x-line,
+//       pointwise            -> F = sigma~ A~^T (qdata A~ = sqrt(mu W) J^{-1}, r = lam/mu),
+//       transposed x         -> V[c][d][i]                                  (sY -> regs -> sY)
+//   Yt: transposed y         -> Wb = By^T V0 + Dy^T V1, Wd = By^T V2        (sY -> sZ)
+//   Zt: transposed z + scatter: y[node] += Bz^T Wb + Dz^T Wd  (red.global.add.f64; skips
+//       Dirichlet rows, whose values the init kernel already set to x)
+//
+// Coefficients of B, D are broadcast from shared memory into REGISTERS: on B200 a DFMA
+// with a constant/uniform-register operand runs at ~20 TF/s against ~34 TF/s with all
+// register operands (tools/microbench); each coefficient feeds 3
+// (or 6) FMAs, one per displacement component.
+#pragma once
+#include "elas_internal.h"
+
+namespace elas {
+
+// ---------------------------------------------------------------------------------------
+// compile-time layout search: minimise 128-byte wavefronts of 64-bit shared accesses
+// (half-warp of 16 lanes, bank = double word mod 16, equal addresses broadcast)
+// ---------------------------------------------------------------------------------------
+constexpr int halfwarp_cost(const int* addr, int n) {
+  int total = 0;
+  for (int h = 0; h < n; h += 16) {
+    int cnt[16] = {0};
+    int worst = 0;
+    for (int l = h; l < h + 16 && l < n; ++l) {
+      bool dup = false;
+      for (int m = h; m < l; ++m)
+        if (addr[m] == addr[l]) dup = true;
+      if (dup) continue;
+      int b = ((addr[l] % 16) + 16) % 16;
+      cnt[b] += 1;
+      if (cnt[b] > worst) worst = cnt[b];
+    }
+    total += worst;
+  }
+  return total;
+}
+
+// a3-stride of the Z buffer: stage Y/Yt lanes are (i fast, a3 slow)
+constexpr int pick_SA(int N, int Q) {
+  int best = N * N, best_cost = 1 << 30;
+  for (int SA = N * N; SA < N * N + 16; ++SA) {
+    int addr[512] = {0};
+    int n = 0;
+    for (int a3 = 0; a3 < Q; ++a3)
+      for (int i = 0; i < N; ++i) addr[n++] = a3 * SA + i;
+    int c = halfwarp_cost(addr, n);
+    if (c < best_cost) { best_cost = c; best = SA; }
+  }
+  return best;
+}
+
+// a2-stride of the Y buffer: stage X lanes are lines L = a3 + Q a2 (a3 fast)
+constexpr int pick_S2(int N, int Q) {
+  int best = Q * N, best_cost = 1 << 30;
+  for (int S2 = Q * N; S2 < Q * N + 16; ++S2) {
+    int addr[512] = {0};
+    int n = 0;
+    for (int a2 = 0; a2 < Q; ++a2)
+      for (int a3 = 0; a3 < Q; ++a3) addr[n++] = a2 * S2 + a3 * N;
+    int c = halfwarp_cost(addr, n);
+    if (c < best_cost) { best_cost = c; best = S2; }
+  }
+  return best;
+}
+
+constexpr int kSmemLimit = 227 * 1024;
+
+template <int P, int Q>
+struct Cfg {
+  static constexpr int N = P + 1;
+  static constexpr int NT = 256;
+  static constexpr int SA = pick_SA(N, Q);
+  static constexpr int ZV = Q * SA;        // variant stride (Zb | Zd)
+  static constexpr int ZC = 2 * ZV;        // component stride
+  static constexpr int ZE = 3 * ZC;        // element stride
+  static constexpr int S2 = pick_S2(N, Q);
+  static constexpr int YV = Q * S2;        // variant stride (Y0 | Y1 | Y2)
+  static constexpr int YC = 3 * YV;        // component stride
+  static constexpr int YE = 3 * YC;        // element stride
+  static constexpr int TAB = 2 * Q * N;    // B then D
+  static constexpr int EB_threads = (NT / (Q * Q)) > 0 ? NT / (Q * Q) : 1;
+  static constexpr int EB_smem = (kSmemLimit / 8 - TAB) / (ZE + YE);
+  static constexpr int EB = EB_threads < EB_smem ? EB_threads : EB_smem;
+  static constexpr size_t smem = 8u * (size_t)(TAB + EB * (ZE + YE));
+  static_assert(EB >= 1, "element does not fit in shared memory");
+};
+
+__device__ __forceinline__ bool is_constrained(int I, int J, int K, const Slab& s) {
+  const uint32_t f = s.faces;
+  return ((f & ELAS_FACE_XMIN) && I == 0) || ((f & ELAS_FACE_XMAX) && I == s.Nx - 1) ||
+         ((f & ELAS_FACE_YMIN) && J == 0) || ((f & ELAS_FACE_YMAX) && J == s.Ny - 1) ||
+         ((f & ELAS_FACE_ZMIN) && K == 0) || ((f & ELAS_FACE_ZMAX) && K == s.Nz - 1);
+}
+
+// sigma~ = r tr(H) I + H + H^T with H = G A~ ; F = sigma~ A~^T   (Voigt-symmetric: 6 unique)
+__device__ __forceinline__ void pointwise(double (&g)[3][3], const double (&A)[9], double r) {
+  double H[3][3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int m = 0; m < 3; ++m) H[c][m] = fma(g[c][2], A[6 + m], fma(g[c][1], A[3 + m], g[c][0] * A[m]));
+  const double s = r * (H[0][0] + H[1][1] + H[2][2]);
+  double S[3][3];
+  S[0][0] = fma(2.0, H[0][0], s);
+  S[1][1] = fma(2.0, H[1][1], s);
+  S[2][2] = fma(2.0, H[2][2], s);
+  S[0][1] = S[1][0] = H[0][1] + H[1][0];
+  S[0][2] = S[2][0] = H[0][2] + H[2][0];
+  S[1][2] = S[2][1] = H[1][2] + H[2][1];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      g[c][d] = fma(S[c][2], A[3 * d + 2], fma(S[c][1], A[3 * d + 1], S[c][0] * A[3 * d]));
+}
+
+template <int P, int Q>
+__global__ void __launch_bounds__(Cfg<P, Q>::NT, 1)
+    apply_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
+                 const double* __restrict__ rr, const double* __restrict__ tables, Slab s,
+                 int64_t e_begin, int64_t e_end) {
+  using C = Cfg<P, Q>;
+  constexpr int N = C::N;
+  constexpr int NT = C::NT;
+  constexpr int EB = C::EB;
+  extern __shared__ double smem[];
+  double* sB = smem;            // B[a][i] = l_i(g_a), Q x N
+  double* sD = smem + Q * N;    // D[a][i] = l_i'(g_a)
+  double* sZ = smem + C::TAB;
+  double* sY = sZ + EB * C::ZE;
+
+  const int tid = threadIdx.x;
+  const int64_t e0 = e_begin + (int64_t)blockIdx.x * EB;
+  const int ne = (int)((e_end - e0) < EB ? (e_end - e0) : EB);
+  for (int t = tid; t < C::TAB; t += NT) sB[t] = tables[t];
+  const int64_t plane = (int64_t)s.Nx * s.Ny;
+  const bool bc = s.faces != 0;
+  __syncthreads();
+
+  // ---------------- Stage Z: gather + contraction in z --------------------------------
+  for (int w = tid; w < ne * N * N; w += NT) {
+    const int i = w % N, j = (w / N) % N, el = w / (N * N);
+    const int64_t e = e0 + el;
+    const int ex = (int)(e % s.nx), ey = (int)((e / s.nx) % s.ny), ez = (int)(e / ((int64_t)s.nx * s.ny));
+    const int I = ex * P + i, J = ey * P + j;
+    const int64_t base = I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
+    double u[3][N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const bool cons = bc && is_constrained(I, J, ez * P + k, s);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) u[c][k] = cons ? 0.0 : __ldg(x + c * s.nodes + base + k * plane);
+    }
+    double* dst = sZ + el * C::ZE + j * N + i;
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+      double zb[3] = {0.0, 0.0, 0.0}, zd[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const double b = sB[a * N + k], d = sD[a * N + k];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          zb[c] = fma(b, u[c][k], zb[c]);
+          zd[c] = fma(d, u[c][k], zd[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        dst[c * C::ZC + a * C::SA] = zb[c];
+        dst[c * C::ZC + C::ZV + a * C::SA] = zd[c];
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---------------- Stage Y: contraction in y ------------------------------------------
+  for (int w = tid; w < ne * Q * N; w += NT) {
+    const int i = w % N, a3 = (w / N) % Q, el = w / (N * Q);
+    const double* src = sZ + el * C::ZE + a3 * C::SA + i;
+    double zb[3][N], zd[3][N];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        zb[c][j] = src[c * C::ZC + j * N];
+        zd[c][j] = src[c * C::ZC + C::ZV + j * N];
+      }
+    double* dst = sY + el * C::YE + a3 * N + i;
+#pragma unroll
+    for (int a2 = 0; a2 < Q; ++a2) {
+      double y0[3] = {0, 0, 0}, y1[3] = {0, 0, 0}, y2[3] = {0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const double b = sB[a2 * N + j], d = sD[a2 * N + j];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          y0[c] = fma(b, zb[c][j], y0[c]);
+          y1[c] = fma(d, zb[c][j], y1[c]);
+          y2[c] = fma(b, zd[c][j], y2[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        dst[c * C::YC + a2 * C::S2] = y0[c];
+        dst[c * C::YC + C::YV + a2 * C::S2] = y1[c];
+        dst[c * C::YC + 2 * C::YV + a2 * C::S2] = y2[c];
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---------------- Stage X + pointwise + transposed X ---------------------------------
+  for (int w = tid; w < ne * Q * Q; w += NT) {
+    const int L = w % (Q * Q), el = w / (Q * Q);
+    const int a3 = L % Q, a2 = L / Q;
+    const int64_t e = e0 + el;
+    double* line = sY + el * C::YE + a2 * C::S2 + a3 * N;
+    double g[3][3][Q];
+#pragma unroll
+    for (int v = 0; v < 3; ++v) {
+      const double* tab = (v == 0) ? sD : sB;
+      double f[3][N];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int i = 0; i < N; ++i) f[c][i] = line[c * C::YC + v * C::YV + i];
+#pragma unroll
+      for (int a1 = 0; a1 < Q; ++a1) {
+        double acc[3] = {0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const double t = tab[a1 * N + i];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) acc[c] = fma(t, f[c][i], acc[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) g[c][v][a1] = acc[c];
+      }
+    }
+    const double r = __ldg(rr + e);
+    const double* qp = qd + e * (int64_t)(9 * Q * Q * Q) + L;
+    double An[9];
+#pragma unroll
+    for (int f = 0; f < 9; ++f) An[f] = __ldg(qp + f * Q * Q);
+#pragma unroll
+    for (int a1 = 0; a1 < Q; ++a1) {
+      double A[9];
+#pragma unroll
+      for (int f = 0; f < 9; ++f) A[f] = An[f];
+      if (a1 + 1 < Q) {
+#pragma unroll
+        for (int f = 0; f < 9; ++f) An[f] = __ldg(qp + ((a1 + 1) * 9 + f) * Q * Q);
+      }
+      double G[3][3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) G[c][d] = g[c][d][a1];
+      pointwise(G, A, r);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) g[c][d][a1] = G[c][d];
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double* tab = (d == 0) ? sD : sB;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double acc[3] = {0, 0, 0};
+#pragma unroll
+        for (int a1 = 0; a1 < Q; ++a1) {
+          const double t = tab[a1 * N + i];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) acc[c] = fma(t, g[c][d][a1], acc[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) line[c * C::YC + d * C::YV + i] = acc[c];
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---------------- Stage Yt: transposed contraction in y ------------------------------
+  for (int w = tid; w < ne * Q * N; w += NT) {
+    const int i = w % N, a3 = (w / N) % Q, el = w / (N * Q);
+    const double* src = sY + el * C::YE + a3 * N + i;
+    double wb[3][N], wd[3][N];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int j = 0; j < N; ++j) wb[c][j] = wd[c][j] = 0.0;
+#pragma unroll
+    for (int a2 = 0; a2 < Q; ++a2) {
+      double v0[3], v1[3], v2[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        v0[c] = src[c * C::YC + a2 * C::S2];
+        v1[c] = src[c * C::YC + C::YV + a2 * C::S2];
+        v2[c] = src[c * C::YC + 2 * C::YV + a2 * C::S2];
+      }
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const double b = sB[a2 * N + j], d = sD[a2 * N + j];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          wb[c][j] = fma(d, v1[c], fma(b, v0[c], wb[c][j]));
+          wd[c][j] = fma(b, v2[c], wd[c][j]);
+        }
+      }
+    }
+    double* dst = sZ + el * C::ZE + a3 * C::SA + i;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        dst[c * C::ZC + j * N] = wb[c][j];
+        dst[c * C::ZC + C::ZV + j * N] = wd[c][j];
+      }
+  }
+  __syncthreads();
+
+  // ---------------- Stage Zt: transposed contraction in z + scatter-add ----------------
+  for (int w = tid; w < ne * N * N; w += NT) {
+    const int i = w % N, j = (w / N) % N, el = w / (N * N);
+    const int64_t e = e0 + el;
+    const int ex = (int)(e % s.nx), ey = (int)((e / s.nx) % s.ny), ez = (int)(e / ((int64_t)s.nx * s.ny));
+    const double* src = sZ + el * C::ZE + j * N + i;
+    double o[3][N];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int k = 0; k < N; ++k) o[c][k] = 0.0;
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+      double wb[3], wd[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        wb[c] = src[c * C::ZC + a * C::SA];
+        wd[c] = src[c * C::ZC + C::ZV + a * C::SA];
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const double b = sB[a * N + k], d = sD[a * N + k];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) o[c][k] = fma(d, wd[c], fma(b, wb[c], o[c][k]));
+      }
+    }
+    const int I = ex * P + i, J = ey * P + j;
+    const int64_t base = I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      if (bc && is_constrained(I, J, ez * P + k, s)) continue;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) atomicAdd(y + c * s.nodes + base + k * plane, o[c][k]);
+    }
+  }
+}
+
+template <int P, int Q>
+cudaError_t launch_apply_pq(const Slab& s, const double* x, double* y, const double* qd,
+                            const double* rr, const double* tables, int64_t e_begin, int64_t e_end,
+                            cudaStream_t st) {
+  using C = Cfg<P, Q>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t err = cudaFuncSetAttribute(apply_kernel<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)C::smem);
+    if (err != cudaSuccess) return err;
+    attr_done = true;
+  }
+  const int64_t ne = e_end - e_begin;
+  if (ne <= 0) return cudaSuccess;
+  const int64_t grid = (ne + C::EB - 1) / C::EB;
+  apply_kernel<P, Q><<<(unsigned)grid, C::NT, C::smem, st>>>(x, y, qd, rr, tables, s, e_begin, e_end);
+  return cudaGetLastError();
+}
+
+template <int P, int Q>
+void info_pq(ApplyLaunch* info) {
+  using C = Cfg<P, Q>;
+  info->threads = C::NT;
+  info->elems_per_cta = C::EB;
+  info->smem_bytes = C::smem;
+}
+
+}  // namespace elas
+
+// Instantiate the two quadrature variants q = p+1, p+2 of one degree P.
+#define ELAS_DEFINE_DEGREE(P)                                                                   \
+  namespace elas {                                                                              \
+  cudaError_t apply_info_p##P(int q, ApplyLaunch* info) {                                       \
+    if (q == P + 1) info_pq<P, P + 1>(info);                                                    \
+    else if (q == P + 2) info_pq<P, P + 2>(info);                                               \
+    else return cudaErrorInvalidValue;                                                          \
+    return cudaSuccess;                                                                         \
+  }                                                                                             \
+  cudaError_t apply_launch_p##P(int q, const Slab& s, const double* x, double* y,               \
+                                const double* qd, const double* rr, const double* tables,       \
+                                int64_t e_begin, int64_t e_end, cudaStream_t st) {              \
+    if (q == P + 1) return launch_apply_pq<P, P + 1>(s, x, y, qd, rr, tables, e_begin, e_end, st); \
+    if (q == P + 2) return launch_apply_pq<P, P + 2>(s, x, y, qd, rr, tables, e_begin, e_end, st); \
+    return cudaErrorInvalidValue;                                                               \
+  }                                                                                             \
+  }

@@ -1,0 +1,3 @@
+// Kernel instances for degree p = 1 (q = p+1 and p+2); see elas_apply.cuh.
+#include "elas_apply.cuh"
+ELAS_DEFINE_DEGREE(1)

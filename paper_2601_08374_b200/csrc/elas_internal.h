@@ -1,0 +1,48 @@
+// Internal declarations shared by the libelas translation units.
+#pragma once
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/elas.h"
+
+namespace elas {
+
+// Everything a kernel needs to address one rank's slab (all LOCAL indices).
+struct Slab {
+  int32_t nx, ny, nz;        // elements per axis (nz = local layers)
+  int32_t Nx, Ny, Nz;        // nodes per axis (Nz = nz p + 1)
+  int64_t nodes;             // Nx * Ny * Nz
+  uint32_t faces;            // Dirichlet face bits, z faces already restricted to this slab
+};
+
+// Launch configuration the host needs for one (p, q) kernel instance.
+struct ApplyLaunch {
+  int threads;               // CTA size
+  int elems_per_cta;         // EB
+  size_t smem_bytes;         // dynamic shared memory
+};
+
+// Host tables (elas_tables.cpp): GLL nodes, Gauss-Legendre rule, barycentric Lagrange.
+int host_tables(int p, int q, double* nodes, double* points, double* weights, double* B, double* D);
+
+// Per-degree translation units (elas_apply_p<P>.cu) export these; q must be p+1 or p+2.
+// Returns cudaSuccess or an error; `info` only queries the configuration.
+cudaError_t apply_info(int p, int q, ApplyLaunch* info);
+cudaError_t apply_launch(int p, int q, const Slab& s, const double* x, double* y, const double* qd,
+                         const double* rr, const double* tables, int64_t e_begin, int64_t e_end,
+                         cudaStream_t st);
+
+// Kernels in elas_setup.cu
+cudaError_t launch_qdata(int p, int q, const Slab& s, const double* verts, const double* lam,
+                         const double* mu, const double* gpts, const double* gw, double* qd,
+                         double* rr, int* bad, cudaStream_t st);
+cudaError_t launch_init(const Slab& s, const double* x, double* y, cudaStream_t st);
+cudaError_t launch_plane_add(const Slab& s, int which_plane, double* y, const double* halo,
+                             cudaStream_t st);
+
+// error helpers
+void set_error(const std::string& msg);
+
+}  // namespace elas

@@ -1,0 +1,141 @@
+// Setup and small per-apply kernels:
+//  * qdata kernel (the "assembly" phase of partial assembly; Alg. 1 inputs
+//    geom.J(p,e), ipWeights[p], lambda(p,e), mu(p,e); Table 3 "Assembly" column):
+//      J_mk = d x_m / d xi_k of the trilinear map (8 vertices) at each Gauss point,
+//      det J (> 0, else ELAS_EGEOM), A = J^{-1}, W = w_a w_b w_c det J,
+//      stored:  A~ = sqrt(mu_e W) A  (9 doubles per point)  and  r_e = lambda_e / mu_e.
+//    With H = G A~ and sigma~ = r tr(H) I + H + H^T,  sigma~ A~^T = W sigma A^T exactly
+//    (DESIGN.md section 5): 9 doubles per point is the minimal stored form.
+//    Layout qd[e][a1][f][L], L = a3 + q a2 (the x-line index of the apply kernel), so the
+//    threads of one warp read consecutive doubles.
+//  * init kernel: y = (I - Z) x  (0 on free dofs, x on Dirichlet dofs) before the atomics.
+//  * plane-add kernel: y_plane += halo on free dofs (multi-GPU interface sum, P^T of
+//    PAPER.md:169).
+#include "elas_internal.h"
+
+namespace elas {
+
+namespace {
+
+__device__ __forceinline__ bool constrained_node(int I, int J, int K, const Slab& s) {
+  const uint32_t f = s.faces;
+  return ((f & ELAS_FACE_XMIN) && I == 0) || ((f & ELAS_FACE_XMAX) && I == s.Nx - 1) ||
+         ((f & ELAS_FACE_YMIN) && J == 0) || ((f & ELAS_FACE_YMAX) && J == s.Ny - 1) ||
+         ((f & ELAS_FACE_ZMIN) && K == 0) || ((f & ELAS_FACE_ZMAX) && K == s.Nz - 1);
+}
+
+struct QParams {
+  double g[16];
+  double w[16];
+};
+
+__global__ void qdata_kernel(int q, Slab s, const double* __restrict__ V, const double* __restrict__ lam,
+                             const double* __restrict__ mu, QParams qp, double* __restrict__ qd,
+                             double* __restrict__ rr, int* __restrict__ bad, int64_t total) {
+  const int q3 = q * q * q;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / q3;
+    const int pt = (int)(t % q3);
+    const int a1 = pt % q, a2 = (pt / q) % q, a3 = pt / (q * q);
+    const int ex = (int)(e % s.nx), ey = (int)((e / s.nx) % s.ny), ez = (int)(e / ((int64_t)s.nx * s.ny));
+    const double xi[3] = {qp.g[a1], qp.g[a2], qp.g[a3]};
+    double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    for (int c = 0; c < 2; ++c)
+      for (int b = 0; b < 2; ++b)
+        for (int a = 0; a < 2; ++a) {
+          const int64_t v = ((int64_t)(ez + c) * (s.ny + 1) + (ey + b)) * (s.nx + 1) + (ex + a);
+          const double h0 = a ? xi[0] : 1.0 - xi[0], d0 = a ? 1.0 : -1.0;
+          const double h1 = b ? xi[1] : 1.0 - xi[1], d1 = b ? 1.0 : -1.0;
+          const double h2 = c ? xi[2] : 1.0 - xi[2], d2 = c ? 1.0 : -1.0;
+          const double dN[3] = {d0 * h1 * h2, h0 * d1 * h2, h0 * h1 * d2};
+          for (int m = 0; m < 3; ++m) {
+            const double X = V[v * 3 + m];
+            for (int k = 0; k < 3; ++k) J[m][k] = fma(X, dN[k], J[m][k]);
+          }
+        }
+    // adjugate / determinant
+    double adj[3][3];
+    adj[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    adj[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+    adj[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+    adj[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    adj[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+    adj[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+    adj[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    adj[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+    adj[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    const double det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
+    if (!(det > 0.0)) {
+      atomicExch(bad, 1);
+      continue;
+    }
+    const double W = qp.w[a1] * qp.w[a2] * qp.w[a3] * det;
+    const double sc = sqrt(mu[e] * W) / det;   // A~ = sqrt(mu W) J^{-1} = sqrt(mu W) adj / det
+    const int L = a3 + q * a2;
+    double* out = qd + e * (int64_t)(9 * q3) + (int64_t)a1 * 9 * q * q + L;
+    for (int d = 0; d < 3; ++d)
+      for (int m = 0; m < 3; ++m) out[(3 * d + m) * q * q] = sc * adj[d][m];
+    if (pt == 0) rr[e] = lam[e] / mu[e];
+  }
+}
+
+__global__ void init_kernel(Slab s, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t n = 3 * s.nodes;
+  const bool bc = s.faces != 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (bc) {
+      const int64_t node = t % s.nodes;
+      const int I = (int)(node % s.Nx), J = (int)((node / s.Nx) % s.Ny), K = (int)(node / ((int64_t)s.Nx * s.Ny));
+      if (constrained_node(I, J, K, s)) v = x[t];
+    }
+    y[t] = v;
+  }
+}
+
+__global__ void plane_add_kernel(Slab s, int K, double* __restrict__ y, const double* __restrict__ halo) {
+  const int64_t plane = (int64_t)s.Nx * s.Ny;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 3 * plane; t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t / plane);
+    const int64_t pidx = t % plane;
+    const int I = (int)(pidx % s.Nx), J = (int)(pidx / s.Nx);
+    if (s.faces && constrained_node(I, J, K, s)) continue;
+    double* dst = y + c * s.nodes + (int64_t)K * plane + pidx;
+    *dst = *dst + halo[t];
+  }
+}
+
+int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  const int64_t cap = 148 * 32;
+  return (int)(g < cap ? (g > 0 ? g : 1) : cap);
+}
+
+}  // namespace
+
+cudaError_t launch_qdata(int p, int q, const Slab& s, const double* verts, const double* lam,
+                         const double* mu, const double* gpts, const double* gw, double* qd,
+                         double* rr, int* bad, cudaStream_t st) {
+  (void)p;
+  QParams qp{};
+  for (int a = 0; a < q; ++a) {
+    qp.g[a] = gpts[a];
+    qp.w[a] = gw[a];
+  }
+  const int64_t total = (int64_t)s.nx * s.ny * s.nz * q * q * q;
+  qdata_kernel<<<grid_for(total, 256), 256, 0, st>>>(q, s, verts, lam, mu, qp, qd, rr, bad, total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init(const Slab& s, const double* x, double* y, cudaStream_t st) {
+  init_kernel<<<grid_for(3 * s.nodes, 256), 256, 0, st>>>(s, x, y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plane_add(const Slab& s, int which_plane, double* y, const double* halo, cudaStream_t st) {
+  const int64_t n = 3 * (int64_t)s.Nx * s.Ny;
+  plane_add_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, which_plane, y, halo);
+  return cudaGetLastError();
+}
+
+}  // namespace elas

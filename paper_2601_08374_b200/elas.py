@@ -1,0 +1,276 @@
+"""Thin ctypes binding of libelas.so (include/elas.h): argument marshalling only.
+
+Every step of the operator runs in the library's CUDA kernels.  There is no CPU fallback:
+if the in-tree library is missing, ``load()`` raises (build it with
+``python -m paper_2601_08374_b200.build`` or ``__graft_entry__.build()``).
+
+Functions mirror the C names (elas_create, elas_apply, ...); ``Operator`` is a small
+convenience wrapper that owns the handle.  Device arrays are passed as torch CUDA tensors
+(or raw integer device pointers); host arrays as numpy float64 arrays.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libelas.so")
+
+ELAS_OK, ELAS_EINVAL, ELAS_EGEOM, ELAS_ENOMEM, ELAS_ECUDA, ELAS_ENCCL = 0, -1, -2, -3, -4, -5
+FACE_XMIN, FACE_XMAX, FACE_YMIN, FACE_YMAX, FACE_ZMIN, FACE_ZMAX = 1, 2, 4, 8, 16, 32
+
+EXPORTED = ["elas_create", "elas_apply", "elas_apply_host", "elas_interface_add", "elas_destroy",
+            "elas_local_dofs", "elas_local_zrange", "elas_set_stream", "elas_launches_per_apply",
+            "elas_last_error", "elas_slab_range", "elas_tables", "elas_nccl_unique_id", "elas_version",
+            "elas_profile", "elas_profile_read"]
+
+
+class ElasError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"elas error {code}: {msg}")
+        self.code = code
+
+
+class elas_mesh(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32),
+                ("vertices", ctypes.POINTER(ctypes.c_double)),
+                ("lx", ctypes.c_double), ("ly", ctypes.c_double), ("lz", ctypes.c_double),
+                ("dirichlet_faces", ctypes.c_uint32), ("material_per_element", ctypes.c_int32),
+                ("nccl_id", ctypes.c_void_p), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def load(path=None):
+    """Load the in-tree libelas.so (raises if it is missing: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or LIB_PATH
+    if not os.path.exists(path):
+        raise ImportError(f"libelas.so not built at {path}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    P, D, I32, I64 = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.c_int64
+    lib.elas_create.restype = P
+    lib.elas_create.argtypes = [ctypes.POINTER(elas_mesh), ctypes.c_int, ctypes.c_int, D, D]
+    lib.elas_apply.restype = ctypes.c_int
+    lib.elas_apply.argtypes = [P, P, P]
+    lib.elas_apply_host.restype = ctypes.c_int
+    lib.elas_apply_host.argtypes = [P, P, P]
+    lib.elas_interface_add.restype = ctypes.c_int
+    lib.elas_interface_add.argtypes = [P, P, P, P]
+    lib.elas_destroy.restype = None
+    lib.elas_destroy.argtypes = [P]
+    lib.elas_local_dofs.restype = I64
+    lib.elas_local_dofs.argtypes = [P]
+    lib.elas_local_zrange.restype = ctypes.c_int
+    lib.elas_local_zrange.argtypes = [P, ctypes.POINTER(I32), ctypes.POINTER(I32)]
+    lib.elas_set_stream.restype = ctypes.c_int
+    lib.elas_set_stream.argtypes = [P, P]
+    lib.elas_launches_per_apply.restype = ctypes.c_int
+    lib.elas_launches_per_apply.argtypes = [P]
+    lib.elas_last_error.restype = ctypes.c_char_p
+    lib.elas_last_error.argtypes = []
+    lib.elas_slab_range.restype = ctypes.c_int
+    lib.elas_slab_range.argtypes = [I32, I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32)]
+    lib.elas_tables.restype = ctypes.c_int
+    lib.elas_tables.argtypes = [ctypes.c_int, ctypes.c_int, D, D, D, D, D]
+    lib.elas_version.restype = ctypes.c_int
+    lib.elas_version.argtypes = []
+    lib.elas_nccl_unique_id.restype = ctypes.c_int
+    lib.elas_nccl_unique_id.argtypes = [P]
+    lib.elas_profile.restype = ctypes.c_int
+    lib.elas_profile.argtypes = [P, ctypes.c_int]
+    lib.elas_profile_read.restype = ctypes.c_int
+    lib.elas_profile_read.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]
+    _lib = lib
+    return lib
+
+
+def _ptr(a):
+    """Device pointer of a torch tensor (or an int pointer)."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return a
+    return a.data_ptr()
+
+
+def _dptr(arr):
+    return arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _check(rc, what):
+    if rc != ELAS_OK:
+        raise ElasError(rc, f"{what}: {elas_last_error()}")
+
+
+# ------------------------------------------------------------------ C-named functions
+
+def elas_last_error():
+    return load().elas_last_error().decode()
+
+
+def elas_version():
+    return load().elas_version()
+
+
+def elas_nccl_unique_id():
+    """A fresh 128-byte ncclUniqueId (bytes) for elas_create(..., nccl_id=...)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load().elas_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)), "elas_nccl_unique_id")
+    return buf.raw
+
+
+def elas_slab_range(nz, rank, nranks):
+    b, e = ctypes.c_int32(), ctypes.c_int32()
+    _check(load().elas_slab_range(nz, rank, nranks, ctypes.byref(b), ctypes.byref(e)), "elas_slab_range")
+    return b.value, e.value
+
+
+def elas_tables(p, q):
+    """(nodes[p+1], points[q], weights[q], B[q,p+1], D[q,p+1]) as the kernels use them."""
+    n = p + 1
+    nodes, pts, w = np.zeros(n), np.zeros(q), np.zeros(q)
+    B, D = np.zeros((q, n)), np.zeros((q, n))
+    _check(load().elas_tables(p, q, _dptr(nodes), _dptr(pts), _dptr(w), _dptr(B), _dptr(D)), "elas_tables")
+    return nodes, pts, w, B, D
+
+
+def elas_create(nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0), faces=0,
+                rank=0, nranks=1, nccl_id=None):
+    """Returns an opaque handle (int).  lam/mu: scalars or (nz, ny, nx) arrays (GLOBAL)."""
+    lib = load()
+    lam_a = np.ascontiguousarray(np.asarray(lam, dtype=np.float64).reshape(-1))
+    mu_a = np.ascontiguousarray(np.asarray(mu, dtype=np.float64).reshape(-1))
+    per_elem = int(lam_a.size > 1 or mu_a.size > 1)
+    if per_elem:
+        ne = nx * ny * nz
+        lam_a = np.ascontiguousarray(np.broadcast_to(lam_a, (ne,)) if lam_a.size == 1 else lam_a)
+        mu_a = np.ascontiguousarray(np.broadcast_to(mu_a, (ne,)) if mu_a.size == 1 else mu_a)
+        if lam_a.size != ne or mu_a.size != ne:
+            raise ValueError("per-element lambda/mu must have nx*ny*nz entries")
+    m = elas_mesh()
+    m.nx, m.ny, m.nz = nx, ny, nz
+    V = None
+    if vertices is not None:
+        V = np.ascontiguousarray(vertices, dtype=np.float64)
+        if V.size != (nx + 1) * (ny + 1) * (nz + 1) * 3:
+            raise ValueError("vertices must have (nz+1)(ny+1)(nx+1)*3 entries")
+        m.vertices = _dptr(V)
+    m.lx, m.ly, m.lz = lengths
+    m.dirichlet_faces = faces
+    m.material_per_element = per_elem
+    idbuf = None
+    if nccl_id is not None:
+        idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        m.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
+    m.rank, m.nranks = rank, nranks
+    h = lib.elas_create(ctypes.byref(m), p, q, _dptr(lam_a), _dptr(mu_a))
+    if not h:
+        raise ElasError(ELAS_EINVAL, f"elas_create: {elas_last_error()}")
+    return h
+
+
+def elas_apply(h, x, y):
+    _check(load().elas_apply(h, _ptr(x), _ptr(y)), "elas_apply")
+
+
+def elas_apply_host(h, x_host, y_host):
+    """x_host / y_host: contiguous float64 numpy arrays or pinned torch CPU tensors."""
+    px = x_host.ctypes.data if isinstance(x_host, np.ndarray) else x_host.data_ptr()
+    py = y_host.ctypes.data if isinstance(y_host, np.ndarray) else y_host.data_ptr()
+    _check(load().elas_apply_host(h, px, py), "elas_apply_host")
+
+
+def elas_interface_add(h, y, lo_halo, hi_halo):
+    _check(load().elas_interface_add(h, _ptr(y), _ptr(lo_halo), _ptr(hi_halo)), "elas_interface_add")
+
+
+def elas_destroy(h):
+    if h:
+        load().elas_destroy(h)
+
+
+def elas_local_dofs(h):
+    return load().elas_local_dofs(h)
+
+
+def elas_local_zrange(h):
+    b, e = ctypes.c_int32(), ctypes.c_int32()
+    _check(load().elas_local_zrange(h, ctypes.byref(b), ctypes.byref(e)), "elas_local_zrange")
+    return b.value, e.value
+
+
+def elas_set_stream(h, stream):
+    """stream: a torch.cuda.Stream, an int cudaStream_t, or None (legacy default)."""
+    s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+    _check(load().elas_set_stream(h, s), "elas_set_stream")
+
+
+def elas_profile(h, enable):
+    _check(load().elas_profile(h, int(bool(enable))), "elas_profile")
+
+
+def elas_profile_read(h):
+    """(summed apply-kernel milliseconds, number of bracketed launches) since the last read."""
+    ms, n = ctypes.c_double(), ctypes.c_int64()
+    _check(load().elas_profile_read(h, ctypes.byref(ms), ctypes.byref(n)), "elas_profile_read")
+    return ms.value, n.value
+
+
+def elas_launches_per_apply(h):
+    return load().elas_launches_per_apply(h)
+
+
+# ------------------------------------------------------------------ convenience wrapper
+
+class Operator:
+    """Owns one elas_op handle.  Applies run on `stream` (default: torch's current stream)."""
+
+    def __init__(self, nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0),
+                 faces=0, rank=0, nranks=1, nccl_id=None, stream=None):
+        self.p, self.q = p, q
+        self.h = elas_create(nx, ny, nz, p, q, lam, mu, vertices, lengths, faces, rank, nranks, nccl_id)
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream()
+        elas_set_stream(self.h, stream)
+        self.local_dofs = elas_local_dofs(self.h)
+        self.zrange = elas_local_zrange(self.h)
+
+    @classmethod
+    def from_problem(cls, P, rank=0, nranks=1, nccl_id=None, stream=None):
+        """Build from a synth.Problem (affine problems pass vertices=NULL)."""
+        V = None if P.vertices is None else P.vertices
+        return cls(P.nx, P.ny, P.nz, P.p, P.q, P.lam, P.mu, V, (P.lx, P.ly, P.lz),
+                   P.dirichlet_faces, rank, nranks, nccl_id, stream)
+
+    def apply(self, x, y):
+        elas_apply(self.h, x, y)
+
+    def apply_host(self, x_host, y_host):
+        elas_apply_host(self.h, x_host, y_host)
+
+    def interface_add(self, y, lo, hi):
+        elas_interface_add(self.h, y, lo, hi)
+
+    def set_stream(self, stream):
+        elas_set_stream(self.h, stream)
+
+    @property
+    def launches_per_apply(self):
+        return elas_launches_per_apply(self.h)
+
+    def close(self):
+        if self.h:
+            elas_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

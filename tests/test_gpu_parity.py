@@ -1,0 +1,300 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Tolerance: relative L2 error <= 1e-12 over all dofs, or over the sampled rows at full size
+(north_star, BASELINE.json).  Near-zero outputs (rigid modes) use the
+scaled absolute form ||A r|| <= tol ||A||_est ||r||.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def torch_mod():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def oracle_mesh(P):
+    lam, mu = P.material_arrays()
+    return oracle.Mesh(P.vertex_array(), P.p, P.q, lam, mu, P.dirichlet_faces)
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def gpu_apply(P, x=None, op=None):
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    own = op is None
+    if own:
+        op = Operator.from_problem(P)
+    xd = torch.from_numpy(np.ascontiguousarray(P.x if x is None else x)).cuda()
+    yd = torch.full_like(xd, np.nan)
+    op.apply(xd, yd)
+    torch.cuda.synchronize()
+    y = yd.cpu().numpy()
+    if own:
+        op.close()
+    return y
+
+
+def sample_rows(P, n, seed, extra=()):
+    rng = np.random.default_rng(seed)
+    rows = rng.choice(P.num_dofs, size=min(n, P.num_dofs), replace=False)
+    return np.unique(np.concatenate([rows, np.asarray(extra, dtype=np.int64)]))
+
+
+def plane_rows(P, K, count, seed):
+    """Rows on global node plane K (all three components), sampled."""
+    Nx, Ny, Nz = P.node_dims
+    N = Nx * Ny * Nz
+    rng = np.random.default_rng(seed)
+    idx = rng.choice(Nx * Ny, size=min(count, Nx * Ny), replace=False)
+    return np.concatenate([c * N + K * Nx * Ny + idx for c in range(3)])
+
+
+# ---------------------------------------------------------------------------------------
+
+def test_config1_full_and_brute_force():
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_config(1)
+    m = oracle_mesh(P)
+    y_ref = oracle.apply(m, P.x)
+    y = gpu_apply(P)
+    assert rel_l2(y, y_ref) <= TOL
+    # brute force: the GPU operator applied to all 375 unit vectors equals the oracle's A
+    A_ref = oracle.assemble_dense(m)
+    op = Operator.from_problem(P)
+    n = P.num_dofs
+    cols = np.zeros((n, n))
+    I = torch.eye(n, dtype=torch.float64, device="cuda")
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    for j in range(n):
+        op.apply(I[j].contiguous(), out)
+        cols[:, j] = out.cpu().numpy()
+    op.close()
+    assert np.abs(cols - A_ref).max() <= 1e-13 * np.abs(A_ref).max()
+
+
+@pytest.mark.parametrize("p", range(1, 9))
+@pytest.mark.parametrize("dq", [1, 2])
+def test_all_degrees_small_mesh(p, dq):
+    """Perturbed trilinear geometry, per-element material, three Dirichlet faces, a ragged
+    element count (3x2x3 = 18 elements: several CTAs plus a partial one for every p)."""
+    P = synth.make_problem("t", 3, 2, 3, p, p + dq, perturb=True, lognormal_material=True,
+                           faces=synth.FACE_XMIN | 8 | 16, seed=100 + p)
+    y_ref = oracle.apply(oracle_mesh(P), P.x)
+    y = gpu_apply(P)
+    assert rel_l2(y, y_ref) <= TOL
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5])
+def test_many_ctas_ragged(p):
+    """More elements than one wave of CTAs per... and a count that is not a multiple of EB."""
+    P = synth.make_problem("t", 7, 5, 3, p, p + 2, lengths=(1.4, 1.0, 0.6), perturb=True,
+                           lognormal_material=True, faces=2 | 4, seed=7 + p)
+    y_ref = oracle.apply(oracle_mesh(P), P.x)
+    assert rel_l2(gpu_apply(P), y_ref) <= TOL
+
+
+@pytest.mark.parametrize("p", range(1, 9))
+def test_single_element(p):
+    P = synth.make_problem("t", 1, 1, 1, p, p + 2, perturb=True, lam=0.3, mu=2.0, seed=3)
+    assert rel_l2(gpu_apply(P), oracle.apply(oracle_mesh(P), P.x)) <= TOL
+
+
+def test_config2_full():
+    P = synth.make_config(2)
+    y_ref = oracle.apply(oracle_mesh(P), P.x)
+    assert rel_l2(gpu_apply(P), y_ref) <= TOL
+
+
+def test_config3_sampled_rows():
+    P = synth.make_config(3)
+    Nx, Ny, Nz = P.node_dims
+    N = Nx * Ny * Nz
+    # random rows + rows on the Dirichlet face x=0 + rows on element-boundary planes
+    face = np.arange(0, N, Nx)[:50]
+    rows = sample_rows(P, 384, 0, extra=np.concatenate([face, N + face, plane_rows(P, 6, 40, 1)]))
+    y = gpu_apply(P)
+    y_ref = oracle.apply_rows(oracle_mesh(P), P.x, rows)
+    assert rel_l2(y[rows], y_ref) <= TOL
+    Z = oracle.constrained_mask(oracle_mesh(P))
+    assert np.array_equal(y[Z], P.x[Z])             # identity rows, bitwise
+
+
+@pytest.mark.parametrize("p", range(1, 9))
+def test_config4_full_size(p):
+    """Full-size config 4 (~50M dofs) in the bench's launch configuration: sampled rows vs the
+    oracle, plus rigid-mode and symmetry properties that hold at any size."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_config(4, p)
+    op = Operator.from_problem(P)
+    x = torch.from_numpy(P.x).cuda()
+    y = torch.empty_like(x)
+    op.apply(x, y)
+    torch.cuda.synchronize()
+    yh = y.cpu().numpy()
+    rows = sample_rows(P, 160 if p >= 7 else 256, p, extra=plane_rows(P, P.p * 3, 16, p))
+    y_ref = oracle.apply_rows(oracle_mesh(P), P.x, rows)
+    assert rel_l2(yh[rows], y_ref) <= TOL
+    # rigid modes at full size: translation and the rotation (-y, x, 0) of the affine grid
+    Nx, Ny, Nz = P.node_dims
+    nodes = oracle.rules.gll_nodes(p)
+    def coords(n_el, L):
+        h = L / n_el
+        return np.concatenate([e * h + h * nodes[:-1] for e in range(n_el)] + [[L]])
+    X = torch.from_numpy(coords(P.nx, 1.0)).cuda()
+    Y = torch.from_numpy(coords(P.ny, 1.0)).cuda()
+    N = Nx * Ny * Nz
+    r = torch.zeros(3 * N, dtype=torch.float64, device="cuda")
+    r.view(3, Nz, Ny, Nx)[0] = -Y.view(1, Ny, 1)
+    r.view(3, Nz, Ny, Nx)[1] = X.view(1, 1, Nx)
+    Ar = torch.empty_like(r)
+    op.apply(r, Ar)
+    norm_est = float(torch.linalg.norm(y) / torch.linalg.norm(x))   # lower bound of ||A||
+    assert float(torch.linalg.norm(Ar)) <= 1e-11 * norm_est * float(torch.linalg.norm(r))
+    # symmetry x^T A z = z^T A x with a second random vector
+    z = torch.rand_like(x) - 0.5
+    Az = torch.empty_like(z)
+    op.apply(z, Az)
+    a, b = float(torch.dot(x, Az)), float(torch.dot(z, y))
+    assert abs(a - b) <= 1e-12 * float(torch.linalg.norm(x) * torch.linalg.norm(Az))
+    op.close()
+
+
+def test_config5_full_size_sampled():
+    """Config 5 (683M dofs) on one GPU: sampled rows incl. every slab-interface plane of the
+    2/4/8-GPU partitions."""
+    P = synth.make_config(5)
+    p = P.p
+    extra = []
+    for nr in (2, 4, 8):
+        for r in range(1, nr):
+            extra.append(plane_rows(P, (r * P.nz // nr) * p, 8, 10 * nr + r))
+    rows = sample_rows(P, 256, 5, extra=np.concatenate(extra))
+    y = gpu_apply(P)
+    y_ref = oracle.apply_rows(oracle_mesh(P), P.x, rows)
+    assert rel_l2(y[rows], y_ref) <= TOL
+
+
+# ---------------------------------------------------------------------------------------
+# semantics, edge cases and error paths
+# ---------------------------------------------------------------------------------------
+
+def test_dirichlet_identity_and_zero():
+    torch = torch_mod()
+    P = synth.make_problem("t", 2, 3, 2, 3, 5, perturb=True, lognormal_material=True, faces=63, seed=1)
+    m = oracle_mesh(P)
+    Z = oracle.constrained_mask(m)
+    e = np.zeros(P.num_dofs)
+    idx = np.flatnonzero(Z)[17]
+    e[idx] = 1.0
+    assert np.array_equal(gpu_apply(P, e), e)
+    assert np.array_equal(gpu_apply(P, np.zeros(P.num_dofs)), np.zeros(P.num_dofs))
+
+
+def test_apply_host_matches_device():
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_problem("t", 4, 3, 5, 4, 6, perturb=True, lognormal_material=True, faces=1, seed=2)
+    op = Operator.from_problem(P)
+    yh = np.empty_like(P.x)
+    op.apply_host(P.x, yh)
+    yd = gpu_apply(P, op=op)
+    op.close()
+    assert rel_l2(yh, yd) <= 1e-15
+    assert rel_l2(yh, oracle.apply(oracle_mesh(P), P.x)) <= TOL
+
+
+def test_nondefault_stream():
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_problem("t", 3, 3, 3, 2, 4, perturb=True, seed=4)
+    s = torch.cuda.Stream()
+    op = Operator.from_problem(P, stream=s)
+    x = torch.from_numpy(P.x).cuda()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        y = torch.empty_like(x)
+        op.apply(x, y)
+    s.synchronize()
+    assert rel_l2(y.cpu().numpy(), oracle.apply(oracle_mesh(P), P.x)) <= TOL
+    op.close()
+
+
+def test_error_paths_on_gpu():
+    torch = torch_mod()
+    from paper_2601_08374_b200 import elas
+    P = synth.make_problem("t", 2, 2, 2, 2, 4, seed=1)
+    V = P.vertex_array().copy()
+    V[1, 1, 1] = V[0, 0, 0] - 0.1                  # invert elements around the centre vertex
+    with pytest.raises(elas.ElasError, match="det J"):
+        elas.elas_create(2, 2, 2, 2, 4, 1.0, 1.0, vertices=V)
+    op = elas.Operator.from_problem(P)
+    x = torch.from_numpy(P.x).cuda()
+    with pytest.raises(elas.ElasError, match="alias"):
+        op.apply(x, x)
+    y = torch.empty(P.num_dofs + 1, dtype=torch.float64, device="cuda")
+    with pytest.raises(elas.ElasError, match="aligned"):
+        op.apply(x, y.data_ptr() + 4)
+    with pytest.raises(elas.ElasError, match="external"):
+        op.interface_add(y, None, None)
+    op.close()
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4, 8])
+def test_slab_loopback_external_exchange(nranks):
+    """P slab operators on ONE GPU in external-exchange mode, interface planes summed with the
+    library's own plane-add kernel: equals the single-GPU apply to 1e-14 relative."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_problem("t", 5, 4, 16, 6, 8, perturb=True, lognormal_material=True,
+                           faces=1 | 16 | 32, seed=33)
+    y_full = gpu_apply(P)
+    Nx, Ny, Nz = P.node_dims
+    plane = Nx * Ny
+    xg = P.x.reshape(3, Nz, Ny, Nx)
+    ops, ys, ks = [], [], []
+    for r in range(nranks):
+        op = Operator.from_problem(P, rank=r, nranks=nranks)
+        b, e = op.zrange
+        K0, K1 = b * P.p, e * P.p
+        xl = torch.from_numpy(np.ascontiguousarray(xg[:, K0:K1 + 1])).cuda().reshape(-1)
+        assert xl.numel() == op.local_dofs
+        yl = torch.empty_like(xl)
+        op.apply(xl, yl)
+        ops.append(op)
+        ys.append(yl)
+        ks.append((K0, K1))
+    torch.cuda.synchronize()
+    # partial planes (copies taken before any add)
+    lo_part = [y.view(3, -1, plane)[:, 0].contiguous() for y in ys]
+    hi_part = [y.view(3, -1, plane)[:, -1].contiguous() for y in ys]
+    for r in range(nranks):
+        lo = hi_part[r - 1] if r > 0 else None
+        hi = lo_part[r + 1] if r < nranks - 1 else None
+        ops[r].interface_add(ys[r], lo, hi)
+    torch.cuda.synchronize()
+    yg = np.empty((3, Nz, plane))
+    for r in range(nranks):
+        K0, K1 = ks[r]
+        yg[:, K0:K1 + 1] = ys[r].view(3, -1, plane).cpu().numpy()
+        if r > 0:   # replicated interface planes are bitwise equal on both sides
+            assert np.array_equal(ys[r].view(3, -1, plane)[:, 0].cpu().numpy(),
+                                  ys[r - 1].view(3, -1, plane)[:, -1].cpu().numpy())
+    for op in ops:
+        op.close()
+    assert rel_l2(yg.reshape(-1), y_full) <= 1e-14
