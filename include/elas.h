@@ -118,7 +118,7 @@ int elas_set_stream(elas_op* op, void* cuda_stream);
 /* Number of kernel launches one elas_apply issues (for the bench's launch accounting). */
 int elas_launches_per_apply(const elas_op* op);
 
-/* Measurement hook (used by bench.py): while enabled, every launch of the fused apply
+/* Measurement hook (used by bench.py): enabling starts a fresh window; while enabled, every launch of the fused apply
  * kernel inside elas_apply is bracketed by CUDA events on the op's stream.
  * elas_profile_read synchronises on the last event, returns the summed kernel time (ms) and
  * the number of bracketed launches since the previous read, and resets the counters.

@@ -13,7 +13,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
-LIB = os.path.join(LIBDIR, "libelas.so")
+LIB = os.path.join(LIBDIR, os.environ.get("ELAS_LIBNAME", "libelas.so"))
+EXTRA = [f"-D{d}" for d in os.environ.get("ELAS_DEFINES", "").split()]
 ROOT = os.path.dirname(HERE)
 INCLUDE = os.path.join(ROOT, "include")
 
@@ -45,12 +46,12 @@ def _digest():
             h.update(name.encode() + f.read())
     with open(os.path.join(INCLUDE, "elas.h"), "rb") as f:
         h.update(f.read())
-    h.update(" ".join(ARCH + NVCC_FLAGS).encode())
+    h.update(" ".join(ARCH + NVCC_FLAGS + EXTRA).encode())
     return h.hexdigest()[:16]
 
 
 def _compile(src, obj, nccl_inc):
-    cmd = ["nvcc", *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-I", nccl_inc, "-c",
+    cmd = ["nvcc", *ARCH, *NVCC_FLAGS, *EXTRA, "-I", INCLUDE, "-I", nccl_inc, "-c",
            os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -61,14 +62,14 @@ def _compile(src, obj, nccl_inc):
 def build(force=False, verbose=False):
     """Compile every CUDA/C++ source for sm_100a and link lib/libelas.so (skips if up to date)."""
     os.makedirs(LIBDIR, exist_ok=True)
-    stamp = os.path.join(LIBDIR, "libelas.stamp")
+    stamp = LIB + ".stamp"
     dig = _digest()
     if not force and os.path.exists(LIB) and os.path.exists(stamp):
         with open(stamp) as f:
             if f.read().strip() == dig:
                 return LIB
     nccl_inc, nccl_lib = _nccl_paths()
-    objdir = os.path.join(LIBDIR, "obj")
+    objdir = os.path.join(LIBDIR, "obj" + os.environ.get("ELAS_LIBNAME", ""))
     os.makedirs(objdir, exist_ok=True)
     srcs = _sources()
     objs = [os.path.join(objdir, s.rsplit(".", 1)[0] + ".o") for s in srcs]
@@ -78,7 +79,7 @@ def build(force=False, verbose=False):
         for f in cf.as_completed(futs):
             src, log = f.result()
             logs[src] = log
-    with open(os.path.join(LIBDIR, "ptxas.log"), "w") as f:
+    with open(LIB + ".ptxas.log", "w") as f:
         for src in sorted(logs):
             f.write(f"== {src}\n{logs[src]}\n")
     tmp = LIB + ".tmp"

@@ -362,8 +362,8 @@ int elas_set_stream(elas_op* op, void* st) {
 
 int elas_profile(elas_op* op, int enable) {
   if (!op) { set_error("elas_profile: NULL op"); return ELAS_EINVAL; }
-  op->prof = enable != 0;
-  op->prof_used = 0;
+  if (enable && !op->prof) op->prof_used = 0;   // enabling starts a fresh window
+  op->prof = enable != 0;                          // disabling keeps it for elas_profile_read
   return ELAS_OK;
 }
 

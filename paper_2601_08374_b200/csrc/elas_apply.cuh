@@ -81,11 +81,18 @@ constexpr int pick_S2(int N, int Q) {
 }
 
 constexpr int kSmemLimit = 227 * 1024;
+#ifndef ELAS_L2_PREFETCH
+#define ELAS_L2_PREFETCH 1
+#endif
+
+#ifndef ELAS_NT
+#define ELAS_NT 128
+#endif
 
 template <int P, int Q>
 struct Cfg {
   static constexpr int N = P + 1;
-  static constexpr int NT = 256;
+  static constexpr int NT = ELAS_NT;
   static constexpr int SA = pick_SA(N, Q);
   static constexpr int ZV = Q * SA;        // variant stride (Zb | Zd)
   static constexpr int ZC = 2 * ZV;        // component stride
@@ -135,7 +142,7 @@ template <int P, int Q>
 __global__ void __launch_bounds__(Cfg<P, Q>::NT, 1)
     apply_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
                  const double* __restrict__ rr, const double* __restrict__ tables, Slab s,
-                 int64_t e_begin, int64_t e_end) {
+                 int64_t e_begin, int64_t e_end, int pref_ctas) {
   using C = Cfg<P, Q>;
   constexpr int N = C::N;
   constexpr int NT = C::NT;
@@ -151,6 +158,20 @@ __global__ void __launch_bounds__(Cfg<P, Q>::NT, 1)
   const int ne = (int)((e_end - e0) < EB ? (e_end - e0) : EB);
   for (int t = tid; t < C::TAB; t += NT) sB[t] = tables[t];
   const int64_t plane = (int64_t)s.Nx * s.Ny;
+#if ELAS_L2_PREFETCH
+  // Pull the quadrature data of the batch that will run one wave later into L2 (TMA bulk
+  // prefetch: no registers or shared memory), so stage X hits L2 instead of HBM.
+  if (tid == 0 && pref_ctas > 0) {
+    const int64_t pe0 = e0 + (int64_t)pref_ctas * EB;
+    if (pe0 < e_end) {
+      const int64_t pne = (e_end - pe0) < EB ? (e_end - pe0) : EB;
+      const uintptr_t a0 = (uintptr_t)(qd + pe0 * (int64_t)(9 * Q * Q * Q));
+      const uintptr_t a1 = a0 + (uintptr_t)(pne * 9 * Q * Q * Q * 8);
+      const uintptr_t lo = a0 & ~(uintptr_t)15, hi = (a1 + 15) & ~(uintptr_t)15;  // 16-B granules
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
+    }
+  }
+#endif
   const bool bc = s.faces != 0;
   __syncthreads();
 
@@ -389,7 +410,15 @@ cudaError_t launch_apply_pq(const Slab& s, const double* x, double* y, const dou
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
   const int64_t grid = (ne + C::EB - 1) / C::EB;
-  apply_kernel<P, Q><<<(unsigned)grid, C::NT, C::smem, st>>>(x, y, qd, rr, tables, s, e_begin, e_end);
+  static int pref = -1;
+  if (pref < 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_kernel<P, Q>, C::NT, C::smem);
+    pref = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  apply_kernel<P, Q><<<(unsigned)grid, C::NT, C::smem, st>>>(x, y, qd, rr, tables, s, e_begin, e_end, pref);
   return cudaGetLastError();
 }
 
