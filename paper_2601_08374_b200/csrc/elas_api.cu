@@ -12,6 +12,12 @@
 
 #define ELAS_VERSION 10000
 
+// AUTO picks the measured-faster variant.
+#ifndef ELAS_AUTO_TENSOR
+#define ELAS_AUTO_TENSOR 0
+#endif
+static constexpr bool kAutoTensor = ELAS_AUTO_TENSOR != 0;
+
 namespace elas {
 
 namespace {
@@ -62,6 +68,7 @@ using elas::set_error;
 
 struct elas_op {
   int p = 0, q = 0, rank = 0, nranks = 1;
+  int variant = ELAS_VARIANT_SIMT;  // resolved kernel variant
   int32_t ez0 = 0, ez1 = 0;
   Slab slab{};
   int device = 0;
@@ -211,7 +218,8 @@ int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* m
       rc = cuda_fail(e, "cudaMemcpy (operator setup)");
       break;
     }
-    if ((e = elas::launch_qdata(p, q, s, dV, dlam, dmu, g.data(), w.data(), op->qd, op->rr, dbad, op->stream)) ||
+    const int layout = op->variant == ELAS_VARIANT_TENSOR ? elas::QD_LAYOUT_TC6 : elas::QD_LAYOUT_LINES;
+    if ((e = elas::launch_qdata(p, q, layout, s, dV, dlam, dmu, g.data(), w.data(), op->qd, op->rr, dbad, op->stream)) ||
         (e = cudaStreamSynchronize(op->stream))) {
       rc = cuda_fail(e, "qdata setup kernel");
       break;
@@ -244,7 +252,9 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
     op->prof_used += 2;
     CUDA_OR(cudaEventRecord(ev0, st), "cudaEventRecord");
   }
-  cudaError_t e = elas::apply_launch(op->p, op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st);
+  cudaError_t e = op->variant == ELAS_VARIANT_TENSOR
+                      ? elas::apply_tc_launch(op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
+                      : elas::apply_launch(op->p, op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st);
   if (e != cudaSuccess) return cuda_fail(e, "apply kernel launch");
   if (op->prof) CUDA_OR(cudaEventRecord(ev1, st), "cudaEventRecord");
   return ELAS_OK;
@@ -284,7 +294,20 @@ int elas_tables(int p, int q, double* nodes, double* points, double* weights, do
 }
 
 elas_op* elas_create(const elas_mesh* m, int p, int q, const double* lambda, const double* mu) {
+  return elas_create_ex(m, p, q, lambda, mu, ELAS_VARIANT_AUTO);
+}
+
+elas_op* elas_create_ex(const elas_mesh* m, int p, int q, const double* lambda, const double* mu, int variant) {
   elas::g_err.clear();
+  if (variant < ELAS_VARIANT_AUTO || variant > ELAS_VARIANT_TENSOR) {
+    set_error("elas_create_ex: unknown variant");
+    return nullptr;
+  }
+  const bool tc_ok = (p == 6 && q == 8);
+  if (variant == ELAS_VARIANT_TENSOR && !tc_ok) {
+    set_error("elas_create_ex: the tensor-core variant exists for p = 6, q = 8 only");
+    return nullptr;
+  }
   if (!m || !lambda || !mu) { set_error("elas_create: NULL mesh/lambda/mu"); return nullptr; }
   if (p < 1 || p > 8) { set_error("elas_create: p must be in [1, 8]"); return nullptr; }
   if (q != p + 1 && q != p + 2) { set_error("elas_create: q must be p+1 or p+2"); return nullptr; }
@@ -304,6 +327,7 @@ elas_op* elas_create(const elas_mesh* m, int p, int q, const double* lambda, con
   elas_op* op = new elas_op();
   op->p = p;
   op->q = q;
+  op->variant = (variant == ELAS_VARIANT_AUTO) ? (tc_ok && kAutoTensor ? ELAS_VARIANT_TENSOR : ELAS_VARIANT_SIMT) : variant;
   op->nranks = m->nranks < 1 ? 1 : m->nranks;
   op->rank = m->rank;
   int32_t b, e;
@@ -381,6 +405,8 @@ int elas_profile_read(elas_op* op, double* ms, int64_t* launches) {
   op->prof_used = 0;
   return ELAS_OK;
 }
+
+int elas_variant(const elas_op* op) { return op ? op->variant : -1; }
 
 int elas_launches_per_apply(const elas_op* op) {
   if (!op) return -1;

@@ -1,0 +1,38 @@
+// Launch wrapper for the FP64 tensor-core (DMMA) kernel, p = 6, q = 8 (elas_apply_tc.cuh).
+#include "elas_apply_tc.cuh"
+
+namespace elas {
+
+cudaError_t apply_tc_info(ApplyLaunch* info) {
+  info->threads = 32 * tc::WPC;
+  info->elems_per_cta = tc::WPC;
+  info->smem_bytes = sizeof(double) * (size_t)tc::WPC * tc::WARP_SMEM;
+  return cudaSuccess;
+}
+
+cudaError_t apply_tc_launch(const Slab& s, const double* x, double* y, const double* qd, const double* rr,
+                            const double* tables, int64_t e_begin, int64_t e_end, cudaStream_t st) {
+  ApplyLaunch L;
+  apply_tc_info(&L);
+  static bool attr = false;
+  static int pref = 0;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc::apply_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)L.smem_bytes);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc::apply_tc_kernel, L.threads, L.smem_bytes);
+    pref = sms * (per_sm > 0 ? per_sm : 1);
+    attr = true;
+  }
+  const int64_t ne = e_end - e_begin;
+  if (ne <= 0) return cudaSuccess;
+  const int64_t grid = (ne + tc::WPC - 1) / tc::WPC;
+  tc::apply_tc_kernel<<<(unsigned)grid, L.threads, L.smem_bytes, st>>>(x, y, qd, rr, tables, s, e_begin, e_end,
+                                                                      pref);
+  return cudaGetLastError();
+}
+
+}  // namespace elas

@@ -34,8 +34,17 @@ cudaError_t apply_launch(int p, int q, const Slab& s, const double* x, double* y
                          const double* rr, const double* tables, int64_t e_begin, int64_t e_end,
                          cudaStream_t st);
 
+// FP64 tensor-core variant (elas_apply_tc.cu), p = 6, q = 8 only.
+cudaError_t apply_tc_info(ApplyLaunch* info);
+cudaError_t apply_tc_launch(const Slab& s, const double* x, double* y, const double* qd, const double* rr,
+                            const double* tables, int64_t e_begin, int64_t e_end, cudaStream_t st);
+
+// qdata layouts: 0 = qd[e][a1][f][a3 + q a2] (SIMT kernel), 1 = fragment order of the tensor-core
+// kernel: qd[e][slice a1/2][r][f][lane], r = 2 (a1 % 2) + a3 % 2, lane = 4 a2 + a3 / 2.
+enum { QD_LAYOUT_LINES = 0, QD_LAYOUT_TC6 = 1 };
+
 // Kernels in elas_setup.cu
-cudaError_t launch_qdata(int p, int q, const Slab& s, const double* verts, const double* lam,
+cudaError_t launch_qdata(int p, int q, int layout, const Slab& s, const double* verts, const double* lam,
                          const double* mu, const double* gpts, const double* gw, double* qd,
                          double* rr, int* bad, cudaStream_t st);
 cudaError_t launch_init(const Slab& s, const double* x, double* y, cudaStream_t st);

@@ -29,7 +29,7 @@ struct QParams {
   double w[16];
 };
 
-__global__ void qdata_kernel(int q, Slab s, const double* __restrict__ V, const double* __restrict__ lam,
+__global__ void qdata_kernel(int q, int layout, Slab s, const double* __restrict__ V, const double* __restrict__ lam,
                              const double* __restrict__ mu, QParams qp, double* __restrict__ qd,
                              double* __restrict__ rr, int* __restrict__ bad, int64_t total) {
   const int q3 = q * q * q;
@@ -71,10 +71,18 @@ __global__ void qdata_kernel(int q, Slab s, const double* __restrict__ V, const 
     }
     const double W = qp.w[a1] * qp.w[a2] * qp.w[a3] * det;
     const double sc = sqrt(mu[e] * W) / det;   // A~ = sqrt(mu W) J^{-1} = sqrt(mu W) adj / det
-    const int L = a3 + q * a2;
-    double* out = qd + e * (int64_t)(9 * q3) + (int64_t)a1 * 9 * q * q + L;
-    for (int d = 0; d < 3; ++d)
-      for (int m = 0; m < 3; ++m) out[(3 * d + m) * q * q] = sc * adj[d][m];
+    if (layout == QD_LAYOUT_TC6) {
+      // fragment order of apply_tc_kernel (q = 8): 32 lanes contiguous per (slice, r, f)
+      const int sl = a1 >> 1, r = 2 * (a1 & 1) + (a3 & 1), lane = 4 * a2 + (a3 >> 1);
+      double* out = qd + e * (int64_t)(9 * q3) + (int64_t)((sl * 4 + r) * 9) * 32 + lane;
+      for (int d = 0; d < 3; ++d)
+        for (int m = 0; m < 3; ++m) out[(3 * d + m) * 32] = sc * adj[d][m];
+    } else {
+      const int L = a3 + q * a2;
+      double* out = qd + e * (int64_t)(9 * q3) + (int64_t)a1 * 9 * q * q + L;
+      for (int d = 0; d < 3; ++d)
+        for (int m = 0; m < 3; ++m) out[(3 * d + m) * q * q] = sc * adj[d][m];
+    }
     if (pt == 0) rr[e] = lam[e] / mu[e];
   }
 }
@@ -113,7 +121,7 @@ int grid_for(int64_t n, int threads) {
 
 }  // namespace
 
-cudaError_t launch_qdata(int p, int q, const Slab& s, const double* verts, const double* lam,
+cudaError_t launch_qdata(int p, int q, int layout, const Slab& s, const double* verts, const double* lam,
                          const double* mu, const double* gpts, const double* gw, double* qd,
                          double* rr, int* bad, cudaStream_t st) {
   (void)p;
@@ -123,7 +131,7 @@ cudaError_t launch_qdata(int p, int q, const Slab& s, const double* verts, const
     qp.w[a] = gw[a];
   }
   const int64_t total = (int64_t)s.nx * s.ny * s.nz * q * q * q;
-  qdata_kernel<<<grid_for(total, 256), 256, 0, st>>>(q, s, verts, lam, mu, qp, qd, rr, bad, total);
+  qdata_kernel<<<grid_for(total, 256), 256, 0, st>>>(q, layout, s, verts, lam, mu, qp, qd, rr, bad, total);
   return cudaGetLastError();
 }
 

@@ -17,13 +17,14 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", os.environ.get("ELAS_LIBNAME", "libelas.so"))
 
+VARIANT_AUTO, VARIANT_SIMT, VARIANT_TENSOR = 0, 1, 2
 ELAS_OK, ELAS_EINVAL, ELAS_EGEOM, ELAS_ENOMEM, ELAS_ECUDA, ELAS_ENCCL = 0, -1, -2, -3, -4, -5
 FACE_XMIN, FACE_XMAX, FACE_YMIN, FACE_YMAX, FACE_ZMIN, FACE_ZMAX = 1, 2, 4, 8, 16, 32
 
 EXPORTED = ["elas_create", "elas_apply", "elas_apply_host", "elas_interface_add", "elas_destroy",
             "elas_local_dofs", "elas_local_zrange", "elas_set_stream", "elas_launches_per_apply",
             "elas_last_error", "elas_slab_range", "elas_tables", "elas_nccl_unique_id", "elas_version",
-            "elas_profile", "elas_profile_read"]
+            "elas_profile", "elas_profile_read", "elas_create_ex", "elas_variant"]
 
 
 class ElasError(RuntimeError):
@@ -55,6 +56,10 @@ def load(path=None):
     P, D, I32, I64 = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.c_int64
     lib.elas_create.restype = P
     lib.elas_create.argtypes = [ctypes.POINTER(elas_mesh), ctypes.c_int, ctypes.c_int, D, D]
+    lib.elas_create_ex.restype = P
+    lib.elas_create_ex.argtypes = [ctypes.POINTER(elas_mesh), ctypes.c_int, ctypes.c_int, D, D, ctypes.c_int]
+    lib.elas_variant.restype = ctypes.c_int
+    lib.elas_variant.argtypes = [P]
     lib.elas_apply.restype = ctypes.c_int
     lib.elas_apply.argtypes = [P, P, P]
     lib.elas_apply_host.restype = ctypes.c_int
@@ -142,6 +147,17 @@ def elas_tables(p, q):
 def elas_create(nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0), faces=0,
                 rank=0, nranks=1, nccl_id=None):
     """Returns an opaque handle (int).  lam/mu: scalars or (nz, ny, nx) arrays (GLOBAL)."""
+    return elas_create_ex(nx, ny, nz, p, q, lam, mu, vertices, lengths, faces, rank, nranks, nccl_id,
+                          VARIANT_AUTO)
+
+
+def elas_variant(h):
+    return load().elas_variant(h)
+
+
+def elas_create_ex(nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0), faces=0,
+                   rank=0, nranks=1, nccl_id=None, variant=VARIANT_AUTO):
+    """elas_create with an explicit kernel variant (VARIANT_AUTO / _SIMT / _TENSOR)."""
     lib = load()
     lam_a = np.ascontiguousarray(np.asarray(lam, dtype=np.float64).reshape(-1))
     mu_a = np.ascontiguousarray(np.asarray(mu, dtype=np.float64).reshape(-1))
@@ -168,7 +184,7 @@ def elas_create(nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0
         idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
         m.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
     m.rank, m.nranks = rank, nranks
-    h = lib.elas_create(ctypes.byref(m), p, q, _dptr(lam_a), _dptr(mu_a))
+    h = lib.elas_create_ex(ctypes.byref(m), p, q, _dptr(lam_a), _dptr(mu_a), int(variant))
     if not h:
         raise ElasError(ELAS_EINVAL, f"elas_create: {elas_last_error()}")
     return h
@@ -231,9 +247,11 @@ class Operator:
     """Owns one elas_op handle.  Applies run on `stream` (default: torch's current stream)."""
 
     def __init__(self, nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0),
-                 faces=0, rank=0, nranks=1, nccl_id=None, stream=None):
+                 faces=0, rank=0, nranks=1, nccl_id=None, stream=None, variant=VARIANT_AUTO):
         self.p, self.q = p, q
-        self.h = elas_create(nx, ny, nz, p, q, lam, mu, vertices, lengths, faces, rank, nranks, nccl_id)
+        self.h = elas_create_ex(nx, ny, nz, p, q, lam, mu, vertices, lengths, faces, rank, nranks,
+                                nccl_id, variant)
+        self.variant = elas_variant(self.h)
         if stream is None:
             import torch
             stream = torch.cuda.current_stream()
@@ -242,11 +260,11 @@ class Operator:
         self.zrange = elas_local_zrange(self.h)
 
     @classmethod
-    def from_problem(cls, P, rank=0, nranks=1, nccl_id=None, stream=None):
+    def from_problem(cls, P, rank=0, nranks=1, nccl_id=None, stream=None, variant=VARIANT_AUTO):
         """Build from a synth.Problem (affine problems pass vertices=NULL)."""
         V = None if P.vertices is None else P.vertices
         return cls(P.nx, P.ny, P.nz, P.p, P.q, P.lam, P.mu, V, (P.lx, P.ly, P.lz),
-                   P.dirichlet_faces, rank, nranks, nccl_id, stream)
+                   P.dirichlet_faces, rank, nranks, nccl_id, stream, variant)
 
     def apply(self, x, y):
         elas_apply(self.h, x, y)

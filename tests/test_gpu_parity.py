@@ -298,3 +298,45 @@ def test_slab_loopback_external_exchange(nranks):
     for op in ops:
         op.close()
     assert rel_l2(yg.reshape(-1), y_full) <= 1e-14
+
+
+# ---------------------------------------------------------------------------------------
+# kernel variants: FP64 tensor-core (DMMA) kernel for p = 6, q = 8 vs the SIMT kernel
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("dims,faces", [((3, 2, 3), 1 | 8 | 16), ((7, 1, 2), 63), ((1, 1, 1), 0), ((4, 3, 5), 2)])
+def test_p6_variants_vs_oracle(variant, dims, faces):
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_problem("t", *dims, 6, 8, perturb=True, lognormal_material=True, faces=faces, seed=50 + variant)
+    op = Operator.from_problem(P, variant=variant)
+    assert op.variant == variant
+    y = gpu_apply(P, op=op)
+    op.close()
+    assert rel_l2(y, oracle.apply(oracle_mesh(P), P.x)) <= TOL
+
+
+def test_p6_variants_agree_at_config3():
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_config(3)
+    ys = []
+    for variant in (1, 2):
+        op = Operator.from_problem(P, variant=variant)
+        ys.append(gpu_apply(P, op=op))
+        op.close()
+    assert rel_l2(ys[1], ys[0]) <= 1e-14
+
+
+def test_tensor_variant_only_for_p6_q8():
+    torch_mod()
+    from paper_2601_08374_b200 import elas
+    with pytest.raises(elas.ElasError, match="tensor-core"):
+        elas.elas_create_ex(2, 2, 2, 4, 6, 1.0, 1.0, variant=elas.VARIANT_TENSOR)
+    h = elas.elas_create_ex(2, 2, 2, 6, 8, 1.0, 1.0, variant=elas.VARIANT_TENSOR)
+    assert elas.elas_variant(h) == elas.VARIANT_TENSOR
+    elas.elas_destroy(h)
+    h = elas.elas_create_ex(2, 2, 2, 6, 7, 1.0, 1.0)
+    assert elas.elas_variant(h) == elas.VARIANT_SIMT
+    elas.elas_destroy(h)
