@@ -4,9 +4,9 @@
 namespace elas {
 
 cudaError_t apply_tc_info(ApplyLaunch* info) {
-  info->threads = 32 * tc::WPC;
-  info->elems_per_cta = tc::WPC;
-  info->smem_bytes = sizeof(double) * (size_t)tc::WPC * tc::WARP_SMEM;
+  info->threads = 64 * tc::EPC;
+  info->elems_per_cta = tc::EPC;
+  info->smem_bytes = sizeof(double) * (size_t)tc::EPC * tc::ELEM_SMEM;
   return cudaSuccess;
 }
 
@@ -29,7 +29,7 @@ cudaError_t apply_tc_launch(const Slab& s, const double* x, double* y, const dou
   }
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
-  const int64_t grid = (ne + tc::WPC - 1) / tc::WPC;
+  const int64_t grid = (ne + tc::EPC - 1) / tc::EPC;
   tc::apply_tc_kernel<<<(unsigned)grid, L.threads, L.smem_bytes, st>>>(x, y, qd, rr, tables, s, e_begin, e_end,
                                                                       pref);
   return cudaGetLastError();

@@ -8,9 +8,10 @@
 // length-8 (points) index is a [16 fibres x K] x [K x 8] MMA: fibres are the M rows, the
 // contracted index is K (7 padded to 8 with zero coefficients), the produced index the 8
 // columns.  Coefficient fragments (B, D and their transposes) live in registers for the whole
-// kernel.  One WARP processes one element; the warp's shared-memory tiles are bounded by
+// kernel.  A PAIR OF WARPS processes one element; the warp's shared-memory tiles are bounded by
 // processing the y/z stages in four slices of two x-points (a1), the GPU form of the paper's
-// "fibers to slices" loop structure.
+// "fibers to slices" loop structure.  Two warps share an element: each
+// does half of the x-stage tiles, two of the four slices, and half of the x-transpose tiles.
 //
 // Fragment layouts (verified on B200 by tools/microbench/dmma_layout.cu), g = lane>>2, t = lane&3:
 //   A 16x4: a0 = A[g][t], a1 = A[g+8][t];  B 4x8: b0 = B[t][g];
@@ -33,23 +34,25 @@ namespace tc {
 
 constexpr int P = 6, Q = 8, N = 7;
 constexpr int NSLICE = 4;
-// UX[c][v][k][j][a1 ^ swz(j)]: a1 stride 1, j stride 8, k stride 68 (= 4 mod 16), v, c
-constexpr int UX_J = 8, UX_K = 68, UX_V = N * UX_K, UX_C = 2 * UX_V, UX_SIZE = 3 * UX_C;
-// U2[c][w][k][a1l][a2]: a2 stride 1, a1l stride 8, k stride 20 (= 4 mod 16), w, c
-constexpr int U2_A = 8, U2_K = 20, U2_W = N * U2_K, U2_C = 3 * U2_W, U2_SIZE = 3 * U2_C;
-constexpr int WARP_SMEM = UX_SIZE + U2_SIZE;  // doubles per warp (element)
-#ifndef ELAS_TC_WPC
-#define ELAS_TC_WPC 6
+// UX[c][v][k][j][a1]: 7 x 8 (j, a1) rows per k, unpadded; a1 XOR-swizzled by (j, k) so that the
+// x-stage pair stores, the y-stage fragment loads and the x-transpose fragment loads are all
+// bank-conflict free (16 distinct double-word banks per half-warp).
+constexpr int UX_J = 8, UX_K = N * UX_J, UX_V = N * UX_K, UX_C = 2 * UX_V, UX_SIZE = 3 * UX_C;
+// U2[c][w][k][a1l][a2] per slice: a2 XOR-swizzled by k, a1l XOR-swizzled by k so the fragment
+// loads of the z stage cover 16 distinct banks.
+constexpr int U2_A = 8, U2_K = 2 * U2_A, U2_W = N * U2_K, U2_C = 3 * U2_W, U2_SIZE = 3 * U2_C;
+#ifndef ELAS_TC_EPC
+#define ELAS_TC_EPC 6
 #endif
-constexpr int WPC = ELAS_TC_WPC;              // warps = elements per CTA
-constexpr int QD_PER_ELEM = 9 * Q * Q * Q;    // 4608 doubles, fragment order (see qdata kernel)
+constexpr int EPC = ELAS_TC_EPC;               // elements per CTA, two warps each
+constexpr int ELEM_SMEM = UX_SIZE + 2 * U2_SIZE;  // doubles per element (one U2 per warp)
+constexpr int QD_PER_ELEM = 9 * Q * Q * Q;     // 4608 doubles, fragment order (see qdata kernel)
 
-__device__ __forceinline__ int swz(int j) { return ((j >> 1) & 1) << 1; }
 __device__ __forceinline__ int ux(int c, int v, int k, int j, int a1) {
-  return c * UX_C + v * UX_V + k * UX_K + j * UX_J + (a1 ^ swz(j));
+  return c * UX_C + v * UX_V + k * UX_K + j * UX_J + (a1 ^ ((((j >> 1) & 1) << 2) | ((k & 1) << 1)));
 }
 __device__ __forceinline__ int u2(int c, int w, int k, int a1l, int a2) {
-  return c * U2_C + w * U2_W + k * U2_K + a1l * U2_A + a2;
+  return c * U2_C + w * U2_W + k * U2_K + ((a1l ^ ((k >> 1) & 1)) << 3) + (a2 ^ (((k ^ (k >> 2)) & 1) << 2));
 }
 
 __device__ __forceinline__ void mma(double (&c)[4], double a0, double a1, double b) {
@@ -87,29 +90,45 @@ __device__ __forceinline__ void pointwise(double (&G)[3][3], const double* A, do
       G[c][d] = fma(S[c][2], A[3 * d + 2], fma(S[c][1], A[3 * d + 1], S[c][0] * A[3 * d]));
 }
 
-__global__ void __launch_bounds__(32 * WPC, 1)
+// Named barrier for the two warps of element `el` (ids 1..EPC; 0 is __syncthreads).
+__device__ __forceinline__ void pair_sync(int el) {
+  asm volatile("bar.sync %0, 64;" ::"r"(el + 1) : "memory");
+}
+
+// fibre f of the x stages -> (c, j, k), f = c*49 + k*7 + j
+__device__ __forceinline__ void fibre(int f, int& c, int& j, int& k) {
+  const int fc = f < 3 * N * N ? f : 0;
+  c = fc / (N * N);
+  const int r = fc % (N * N);
+  j = r % N;
+  k = r / N;
+}
+
+__global__ void __launch_bounds__(64 * EPC, 1)
     apply_tc_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
                     const double* __restrict__ rr, const double* __restrict__ tables, Slab s,
                     int64_t e_begin, int64_t e_end, int pref_ctas) {
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int el = warp >> 1, half = warp & 1;
   const int g = lane >> 2, t = lane & 3;
-  const int64_t cta_e0 = e_begin + (int64_t)blockIdx.x * WPC;
-  const int64_t e = cta_e0 + warp;
+  const int64_t cta_e0 = e_begin + (int64_t)blockIdx.x * EPC;
+  const int64_t e = cta_e0 + el;
 #if ELAS_L2_PREFETCH
   if (threadIdx.x == 0 && pref_ctas > 0) {
-    const int64_t pe0 = cta_e0 + (int64_t)pref_ctas * WPC;
+    // TMA bulk prefetch into L2 of the qdata of the CTA one wave ahead
+    const int64_t pe0 = cta_e0 + (int64_t)pref_ctas * EPC;
     if (pe0 < e_end) {
-      const int64_t pne = (e_end - pe0) < WPC ? (e_end - pe0) : WPC;
+      const int64_t pne = (e_end - pe0) < EPC ? (e_end - pe0) : EPC;
       const uintptr_t a0 = (uintptr_t)(qd + pe0 * (int64_t)QD_PER_ELEM);
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0),
                    "r"((uint32_t)(pne * QD_PER_ELEM * 8)) : "memory");
     }
   }
 #endif
-  if (e >= e_end) return;
-  double* UX = smem + warp * WARP_SMEM;
-  double* U2 = UX + UX_SIZE;
+  if (e >= e_end) return;  // both warps of an element exit together
+  double* UX = smem + el * ELEM_SMEM;
+  double* U2 = UX + UX_SIZE + half * U2_SIZE;
 
   // coefficient fragments (registers, whole kernel).  tables = B[a][i] (Q x N) then D.
   const double* TB = tables;
@@ -134,55 +153,53 @@ __global__ void __launch_bounds__(32 * WPC, 1)
   const int I0 = ex * P, J0 = ey * P, K0 = ez * P;
   const int64_t ebase = I0 + (int64_t)s.Nx * J0 + plane * K0;
 
-  // ---------------- XF: gather + contraction in x ------------------------------------
-#pragma unroll 2
-  for (int T = 0; T < 10; ++T) {
-    double a[2][2];
-    int fr[2], jj[2], kk[2], cc[2];
+  // ---------------- XF: gather + contraction in x (tiles T = half, half+2, ...) ----------
+  {
+    double a[5][2][2];  // all gathers of this warp issued before any MMA
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int f = 16 * T + g + 8 * h;
-      fr[h] = f;
-      const int fc = f < 3 * N * N ? f : 0;
-      cc[h] = fc / (N * N);
-      const int r = fc % (N * N);
-      jj[h] = r % N;
-      kk[h] = r / N;
-    }
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks)
+    for (int u = 0; u < 5; ++u)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int i = 4 * ks + t;
-        double v = 0.0;
-        if (fr[h] < 3 * N * N && i < N) {
-          const bool z = bc && cons(I0 + i, J0 + jj[h], K0 + kk[h], s);
-          if (!z) v = __ldg(x + cc[h] * s.nodes + ebase + i + (int64_t)s.Nx * jj[h] + plane * kk[h]);
+        const int f = 16 * (2 * u + half) + g + 8 * h;
+        int c, j, k;
+        fibre(f, c, j, k);
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const int i = 4 * ks + t;
+          double v = 0.0;
+          if (f < 3 * N * N && i < N && !(bc && cons(I0 + i, J0 + j, K0 + k, s)))
+            v = __ldg(x + c * s.nodes + ebase + i + (int64_t)s.Nx * j + plane * k);
+          a[u][ks][h] = v;
         }
-        a[ks][h] = v;
       }
-    double cb[4] = {0, 0, 0, 0}, cd[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      mma(cb, a[ks][0], a[ks][1], FB[ks]);
-      mma(cd, a[ks][0], a[ks][1], FD[ks]);
-    }
+    for (int u = 0; u < 5; ++u) {
+      double cb[4] = {0, 0, 0, 0}, cd[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (fr[h] < 3 * N * N) {
-        UX[ux(cc[h], 0, kk[h], jj[h], 2 * t)] = cb[2 * h];
-        UX[ux(cc[h], 0, kk[h], jj[h], 2 * t + 1)] = cb[2 * h + 1];
-        UX[ux(cc[h], 1, kk[h], jj[h], 2 * t)] = cd[2 * h];
-        UX[ux(cc[h], 1, kk[h], jj[h], 2 * t + 1)] = cd[2 * h + 1];
+      for (int ks = 0; ks < 2; ++ks) {
+        mma(cb, a[u][ks][0], a[u][ks][1], FB[ks]);
+        mma(cd, a[u][ks][0], a[u][ks][1], FD[ks]);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int f = 16 * (2 * u + half) + g + 8 * h;
+        if (f < 3 * N * N) {
+          int c, j, k;
+          fibre(f, c, j, k);
+          *reinterpret_cast<double2*>(UX + ux(c, 0, k, j, 2 * t)) = make_double2(cb[2 * h], cb[2 * h + 1]);
+          *reinterpret_cast<double2*>(UX + ux(c, 1, k, j, 2 * t)) = make_double2(cd[2 * h], cd[2 * h + 1]);
+        }
       }
     }
   }
-  __syncwarp();
+  pair_sync(el);
 
   const double re = __ldg(rr + e);
   const double* qe = qd + e * (int64_t)QD_PER_ELEM;
 
-  for (int sl = 0; sl < NSLICE; ++sl) {
+#pragma unroll 1
+  for (int ss = 0; ss < 2; ++ss) {
+    const int sl = 2 * half + ss;   // this warp's slices: a1 in {2 sl, 2 sl + 1}
     // qdata of this slice: 4 points x 9 values per lane, issued early (consumed after ZF)
     double Aq[4][9];
 #pragma unroll
@@ -215,12 +232,9 @@ __global__ void __launch_bounds__(32 * WPC, 1)
       for (int h = 0; h < 2; ++h) {
         const int ff = g + 8 * h, k = ff >> 1, a1l = ff & 1;
         if (ff < 2 * N) {
-          double2* p0 = reinterpret_cast<double2*>(U2 + u2(c, 0, k, a1l, 2 * t));
-          double2* p1 = reinterpret_cast<double2*>(U2 + u2(c, 1, k, a1l, 2 * t));
-          double2* p2 = reinterpret_cast<double2*>(U2 + u2(c, 2, k, a1l, 2 * t));
-          *p0 = make_double2(w0[2 * h], w0[2 * h + 1]);
-          *p1 = make_double2(w1[2 * h], w1[2 * h + 1]);
-          *p2 = make_double2(w2[2 * h], w2[2 * h + 1]);
+          *reinterpret_cast<double2*>(U2 + u2(c, 0, k, a1l, 2 * t)) = make_double2(w0[2 * h], w0[2 * h + 1]);
+          *reinterpret_cast<double2*>(U2 + u2(c, 1, k, a1l, 2 * t)) = make_double2(w1[2 * h], w1[2 * h + 1]);
+          *reinterpret_cast<double2*>(U2 + u2(c, 2, k, a1l, 2 * t)) = make_double2(w2[2 * h], w2[2 * h + 1]);
         }
       }
     }
@@ -314,20 +328,19 @@ __global__ void __launch_bounds__(32 * WPC, 1)
     }
     __syncwarp();
   }
+  pair_sync(el);
 
-  // ---------------- XB: transposed x + scatter-add ---------------------------------------
-#pragma unroll 2
-  for (int T = 0; T < 10; ++T) {
-    int fr[2], jj[2], kk[2], cc[2];
+  // ---------------- XB: transposed x + scatter-add (tiles T = half, half+2, ...) ---------
+#pragma unroll
+  for (int u = 0; u < 5; ++u) {
+    const int T = 2 * u + half;
+    int cc[2], jj[2], kk[2];
+    bool okr[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int f = 16 * T + g + 8 * h;
-      fr[h] = f;
-      const int fc = f < 3 * N * N ? f : 0;
-      cc[h] = fc / (N * N);
-      const int r = fc % (N * N);
-      jj[h] = r % N;
-      kk[h] = r / N;
+      okr[h] = f < 3 * N * N;
+      fibre(f, cc[h], jj[h], kk[h]);
     }
     double o[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -336,22 +349,21 @@ __global__ void __launch_bounds__(32 * WPC, 1)
       double p0[2], p1[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const bool ok = fr[h] < 3 * N * N;
-        p0[h] = ok ? UX[ux(cc[h], 0, kk[h], jj[h], a1)] : 0.0;
-        p1[h] = ok ? UX[ux(cc[h], 1, kk[h], jj[h], a1)] : 0.0;
+        p0[h] = okr[h] ? UX[ux(cc[h], 0, kk[h], jj[h], a1)] : 0.0;
+        p1[h] = okr[h] ? UX[ux(cc[h], 1, kk[h], jj[h], a1)] : 0.0;
       }
       mma(o, p0[0], p0[1], BD[ks]);   // Dx^T T0
       mma(o, p1[0], p1[1], BB[ks]);   // Bx^T T1
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      if (fr[h] >= 3 * N * N) continue;
+      if (!okr[h]) continue;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int i = 2 * t + u;
+      for (int uu = 0; uu < 2; ++uu) {
+        const int i = 2 * t + uu;
         if (i >= N) continue;
         if (bc && cons(I0 + i, J0 + jj[h], K0 + kk[h], s)) continue;
-        atomicAdd(y + cc[h] * s.nodes + ebase + i + (int64_t)s.Nx * jj[h] + plane * kk[h], o[2 * h + u]);
+        atomicAdd(y + cc[h] * s.nodes + ebase + i + (int64_t)s.Nx * jj[h] + plane * kk[h], o[2 * h + uu]);
       }
     }
   }
