@@ -197,7 +197,8 @@ int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* m
     cudaFree(dbad);
   };
   cudaError_t e;
-  const size_t qbytes = sizeof(double) * 9 * (size_t)q * q * q * (size_t)ne;
+  const int qlayout = op->variant == ELAS_VARIANT_TENSOR ? elas::QD_LAYOUT_TC6 : elas::QD_LAYOUT_LINES;
+  const size_t qbytes = sizeof(double) * (size_t)elas::qd_stride(q, qlayout) * (size_t)ne;
   if ((e = cudaMalloc(&op->qd, qbytes)) != cudaSuccess ||
       (e = cudaMalloc(&op->rr, sizeof(double) * ne)) != cudaSuccess ||
       (e = cudaMalloc(&op->tab, sizeof(double) * tabh.size())) != cudaSuccess ||
@@ -218,8 +219,7 @@ int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* m
       rc = cuda_fail(e, "cudaMemcpy (operator setup)");
       break;
     }
-    const int layout = op->variant == ELAS_VARIANT_TENSOR ? elas::QD_LAYOUT_TC6 : elas::QD_LAYOUT_LINES;
-    if ((e = elas::launch_qdata(p, q, layout, s, dV, dlam, dmu, g.data(), w.data(), op->qd, op->rr, dbad, op->stream)) ||
+    if ((e = elas::launch_qdata(p, q, qlayout, s, dV, dlam, dmu, g.data(), w.data(), op->qd, op->rr, dbad, op->stream)) ||
         (e = cudaStreamSynchronize(op->stream))) {
       rc = cuda_fail(e, "qdata setup kernel");
       break;

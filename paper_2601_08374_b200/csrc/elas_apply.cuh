@@ -81,6 +81,16 @@ constexpr int pick_S2(int N, int Q) {
 }
 
 constexpr int kSmemLimit = 227 * 1024;
+#ifndef ELAS_EB_BY_COLUMNS
+#define ELAS_EB_BY_COLUMNS 0
+#endif
+#ifndef ELAS_QD_STAGING
+#define ELAS_QD_STAGING 1
+#endif
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
 #ifndef ELAS_L2_PREFETCH
 #define ELAS_L2_PREFETCH 1
 #endif
@@ -102,10 +112,19 @@ struct Cfg {
   static constexpr int YC = 3 * YV;        // component stride
   static constexpr int YE = 3 * YC;        // element stride
   static constexpr int TAB = 2 * Q * N;    // B then D
-  static constexpr int EB_threads = (NT / (Q * Q)) > 0 ? NT / (Q * Q) : 1;
+  // elements per CTA: enough x-lines for every thread in stage X; at low order also enough
+  // z-columns (N^2 per element) to keep every thread busy in stages Z and Zt.
+  static constexpr int EB_lines = (NT / (Q * Q)) > 0 ? NT / (Q * Q) : 1;
+  static constexpr int EB_cols = (NT + N * N - 1) / (N * N);
+  static constexpr int EB_threads = (ELAS_EB_BY_COLUMNS && EB_cols > EB_lines) ? EB_cols : EB_lines;
   static constexpr int EB_smem = (kSmemLimit / 8 - TAB) / (ZE + YE);
   static constexpr int EB = EB_threads < EB_smem ? EB_threads : EB_smem;
-  static constexpr size_t smem = 8u * (size_t)(TAB + EB * (ZE + YE));
+  static constexpr int QDE = qd_stride_lines(Q);             // qdata doubles per element
+  static constexpr int BASE = (TAB + EB * (ZE + YE) + 1) & ~1;  // 16-B aligned start of sQ
+  // Stage the CTA's quadrature data into shared memory with one TMA bulk copy when two CTAs
+  // per SM still fit (latency of the qdata stream then overlaps stages Z and Y).
+  static constexpr bool STAGE_QD = ELAS_QD_STAGING && 8u * (size_t)(BASE + EB * QDE) + 16 <= (size_t)kSmemLimit / 2;
+  static constexpr size_t smem = STAGE_QD ? 8u * (size_t)(BASE + EB * QDE) + 16 : 8u * (size_t)(TAB + EB * (ZE + YE));
   static_assert(EB >= 1, "element does not fit in shared memory");
 };
 
@@ -152,10 +171,25 @@ __global__ void __launch_bounds__(Cfg<P, Q>::NT, 1)
   double* sD = smem + Q * N;    // D[a][i] = l_i'(g_a)
   double* sZ = smem + C::TAB;
   double* sY = sZ + EB * C::ZE;
+  double* sQ = smem + C::BASE;                                      // staged qdata (STAGE_QD)
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + C::BASE + EB * C::QDE);
 
   const int tid = threadIdx.x;
   const int64_t e0 = e_begin + (int64_t)blockIdx.x * EB;
   const int ne = (int)((e_end - e0) < EB ? (e_end - e0) : EB);
+  if constexpr (C::STAGE_QD) {
+    if (tid == 0) {
+      const uint32_t bar = smem_u32(mbar);
+      const uint32_t bytes = (uint32_t)(8 * ne * C::QDE);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(sQ)),
+          "l"(qd + e0 * (int64_t)C::QDE), "r"(bytes), "r"(bar)
+          : "memory");
+    }
+  }
   for (int t = tid; t < C::TAB; t += NT) sB[t] = tables[t];
   const int64_t plane = (int64_t)s.Nx * s.Ny;
 #if ELAS_L2_PREFETCH
@@ -165,8 +199,8 @@ __global__ void __launch_bounds__(Cfg<P, Q>::NT, 1)
     const int64_t pe0 = e0 + (int64_t)pref_ctas * EB;
     if (pe0 < e_end) {
       const int64_t pne = (e_end - pe0) < EB ? (e_end - pe0) : EB;
-      const uintptr_t a0 = (uintptr_t)(qd + pe0 * (int64_t)(9 * Q * Q * Q));
-      const uintptr_t a1 = a0 + (uintptr_t)(pne * 9 * Q * Q * Q * 8);
+      const uintptr_t a0 = (uintptr_t)(qd + pe0 * (int64_t)C::QDE);
+      const uintptr_t a1 = a0 + (uintptr_t)(pne * C::QDE * 8);
       const uintptr_t lo = a0 & ~(uintptr_t)15, hi = (a1 + 15) & ~(uintptr_t)15;  // 16-B granules
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
     }
@@ -248,6 +282,12 @@ __global__ void __launch_bounds__(Cfg<P, Q>::NT, 1)
   __syncthreads();
 
   // ---------------- Stage X + pointwise + transposed X ---------------------------------
+  if constexpr (C::STAGE_QD) {
+    const uint32_t bar = smem_u32(mbar);
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(bar)
+        : "memory");
+  }
   for (int w = tid; w < ne * Q * Q; w += NT) {
     const int L = w % (Q * Q), el = w / (Q * Q);
     const int a3 = L % Q, a2 = L / Q;
@@ -276,10 +316,10 @@ __global__ void __launch_bounds__(Cfg<P, Q>::NT, 1)
       }
     }
     const double r = __ldg(rr + e);
-    const double* qp = qd + e * (int64_t)(9 * Q * Q * Q) + L;
+    const double* qp = C::STAGE_QD ? sQ + el * C::QDE + L : qd + e * (int64_t)C::QDE + L;
     double An[9];
 #pragma unroll
-    for (int f = 0; f < 9; ++f) An[f] = __ldg(qp + f * Q * Q);
+    for (int f = 0; f < 9; ++f) An[f] = qp[f * Q * Q];
 #pragma unroll
     for (int a1 = 0; a1 < Q; ++a1) {
       double A[9];
@@ -287,7 +327,7 @@ __global__ void __launch_bounds__(Cfg<P, Q>::NT, 1)
       for (int f = 0; f < 9; ++f) A[f] = An[f];
       if (a1 + 1 < Q) {
 #pragma unroll
-        for (int f = 0; f < 9; ++f) An[f] = __ldg(qp + ((a1 + 1) * 9 + f) * Q * Q);
+        for (int f = 0; f < 9; ++f) An[f] = qp[((a1 + 1) * 9 + f) * Q * Q];
       }
       double G[3][3];
 #pragma unroll

@@ -43,6 +43,11 @@ cudaError_t apply_tc_launch(const Slab& s, const double* x, double* y, const dou
 // kernel: qd[e][slice a1/2][r][f][lane], r = 2 (a1 % 2) + a3 % 2, lane = 4 a2 + a3 / 2.
 enum { QD_LAYOUT_LINES = 0, QD_LAYOUT_TC6 = 1 };
 
+// qdata doubles per element: 9 q^3 rounded up to even so every element starts 16-B aligned
+// (TMA bulk copies need 16-B aligned addresses and sizes).
+constexpr int qd_stride_lines(int q) { return (9 * q * q * q + 1) & ~1; }
+inline int qd_stride(int q, int layout) { return layout == QD_LAYOUT_TC6 ? 9 * q * q * q : qd_stride_lines(q); }
+
 // Kernels in elas_setup.cu
 cudaError_t launch_qdata(int p, int q, int layout, const Slab& s, const double* verts, const double* lam,
                          const double* mu, const double* gpts, const double* gw, double* qd,
