@@ -48,11 +48,12 @@ constexpr int EPC = ELAS_TC_EPC;               // elements per CTA, two warps ea
 constexpr int ELEM_SMEM = UX_SIZE + 2 * U2_SIZE;  // doubles per element (one U2 per warp)
 constexpr int QD_PER_ELEM = 9 * Q * Q * Q;     // 4608 doubles, fragment order (see qdata kernel)
 
-__device__ __forceinline__ int ux(int c, int v, int k, int j, int a1) {
-  return c * UX_C + v * UX_V + k * UX_K + j * UX_J + (a1 ^ ((((j >> 1) & 1) << 2) | ((k & 1) << 1)));
+// swizzled offsets inside one (c, v) block of UX / one (c, w) block of U2
+__device__ __forceinline__ int uxo(int k, int j, int a1) {
+  return k * UX_K + j * UX_J + (a1 ^ ((((j >> 1) & 1) << 2) | ((k & 1) << 1)));
 }
-__device__ __forceinline__ int u2(int c, int w, int k, int a1l, int a2) {
-  return c * U2_C + w * U2_W + k * U2_K + ((a1l ^ ((k >> 1) & 1)) << 3) + (a2 ^ (((k ^ (k >> 2)) & 1) << 2));
+__device__ __forceinline__ int u2o(int k, int a1l, int a2) {
+  return k * U2_K + ((a1l ^ ((k >> 1) & 1)) << 3) + (a2 ^ (((k ^ (k >> 2)) & 1) << 2));
 }
 
 __device__ __forceinline__ void mma(double (&c)[4], double a0, double a1, double b) {
@@ -95,13 +96,14 @@ __device__ __forceinline__ void pair_sync(int el) {
   asm volatile("bar.sync %0, 64;" ::"r"(el + 1) : "memory");
 }
 
-// fibre f of the x stages -> (c, j, k), f = c*49 + k*7 + j
+// fibre f of the x stages -> (c, j, k), f = c*49 + k*7 + j; rows past the last fibre are
+// clamped onto it (their results are never stored; padding columns meet zero coefficients)
 __device__ __forceinline__ void fibre(int f, int& c, int& j, int& k) {
-  const int fc = f < 3 * N * N ? f : 0;
+  const int fc = f < 3 * N * N ? f : 3 * N * N - 1;
   c = fc / (N * N);
-  const int r = fc % (N * N);
-  j = r % N;
+  const int r = fc - c * (N * N);
   k = r / N;
+  j = r - k * N;
 }
 
 __global__ void __launch_bounds__(64 * EPC, 1)
@@ -152,6 +154,7 @@ __global__ void __launch_bounds__(64 * EPC, 1)
   const bool bc = s.faces != 0;
   const int I0 = ex * P, J0 = ey * P, K0 = ez * P;
   const int64_t ebase = I0 + (int64_t)s.Nx * J0 + plane * K0;
+  const int iK[2] = {t, (4 + t) < N ? 4 + t : N - 1};   // K index 4 ks + t, clamped (zero coefficient)
 
   // ---------------- XF: gather + contraction in x (tiles T = half, half+2, ...) ----------
   {
@@ -160,16 +163,13 @@ __global__ void __launch_bounds__(64 * EPC, 1)
     for (int u = 0; u < 5; ++u)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int f = 16 * (2 * u + half) + g + 8 * h;
         int c, j, k;
-        fibre(f, c, j, k);
+        fibre(16 * (2 * u + half) + g + 8 * h, c, j, k);
+        const double* src = x + c * s.nodes + ebase + (int64_t)s.Nx * j + plane * k;
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
-          const int i = 4 * ks + t;
-          double v = 0.0;
-          if (f < 3 * N * N && i < N && !(bc && cons(I0 + i, J0 + j, K0 + k, s)))
-            v = __ldg(x + c * s.nodes + ebase + i + (int64_t)s.Nx * j + plane * k);
-          a[u][ks][h] = v;
+          const double v = __ldg(src + iK[ks]);
+          a[u][ks][h] = (bc && cons(I0 + iK[ks], J0 + j, K0 + k, s)) ? 0.0 : v;
         }
       }
 #pragma unroll
@@ -183,15 +183,36 @@ __global__ void __launch_bounds__(64 * EPC, 1)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int f = 16 * (2 * u + half) + g + 8 * h;
+        int c, j, k;
+        fibre(f, c, j, k);
+        double* dst = UX + c * UX_C + uxo(k, j, 2 * t);
         if (f < 3 * N * N) {
-          int c, j, k;
-          fibre(f, c, j, k);
-          *reinterpret_cast<double2*>(UX + ux(c, 0, k, j, 2 * t)) = make_double2(cb[2 * h], cb[2 * h + 1]);
-          *reinterpret_cast<double2*>(UX + ux(c, 1, k, j, 2 * t)) = make_double2(cd[2 * h], cd[2 * h + 1]);
+          *reinterpret_cast<double2*>(dst) = make_double2(cb[2 * h], cb[2 * h + 1]);
+          *reinterpret_cast<double2*>(dst + UX_V) = make_double2(cd[2 * h], cd[2 * h + 1]);
         }
       }
     }
   }
+
+  // lane constants of the slice stages (rows ff = g + 8h -> k = ff >> 1, a1l = ff & 1)
+  const int gl = g & 1, gh = g >> 1;
+  const int kr[2] = {gh, (gh + 4) < N ? gh + 4 : N - 1};
+  const bool row1 = g + 8 < 2 * N;
+  const int sw_yf = (((t >> 1) & 1) << 2) | ((gh & 1) << 1);  // UX swizzle of (j = 4ks+t, k = kr[h])
+  const int sw_yb = ((t & 1) << 2) | ((gh & 1) << 1);         // UX swizzle of (j = 2t+u, k = kr[h])
+  int yfb[2][2], ybl[2][2], zfl[2][2], zbs[2][2], ybs[2][2], yfs[2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      yfb[a][h] = kr[h] * UX_K + iK[a] * UX_J + gl;          // YF load, a = ks
+      ybl[a][h] = u2o(kr[h], gl, 4 * a + t);                   // YB load, a = ks
+      zfl[a][h] = u2o(iK[a], h, g);                            // ZF load, a = ks
+      zbs[a][h] = u2o((2 * t + a) < N ? 2 * t + a : N - 1, h, g);  // ZB store, a = u (k = 2t+u)
+      ybs[a][h] = kr[h] * UX_K + (2 * t + a) * UX_J + gl;      // YB store, a = u (j = 2t+u)
+    }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) yfs[h] = u2o(kr[h], gl, 2 * t);
   pair_sync(el);
 
   const double re = __ldg(rr + e);
@@ -200,41 +221,35 @@ __global__ void __launch_bounds__(64 * EPC, 1)
 #pragma unroll 1
   for (int ss = 0; ss < 2; ++ss) {
     const int sl = 2 * half + ss;   // this warp's slices: a1 in {2 sl, 2 sl + 1}
+    const int xyf = (2 * sl) ^ sw_yf, xyb = (2 * sl) ^ sw_yb;
     // qdata of this slice: 4 points x 9 values per lane, issued early (consumed after ZF)
     double Aq[4][9];
+    const double* qs = qe + sl * 4 * 9 * 32 + lane;
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
-      for (int f = 0; f < 9; ++f) Aq[r][f] = __ldg(qe + ((sl * 4 + r) * 9 + f) * 32 + lane);
+      for (int f = 0; f < 9; ++f) Aq[r][f] = __ldg(qs + (r * 9 + f) * 32);
 
     // ---------------- YF: contraction in y (fibres ff = 2k + a1l, 14 of 16 rows) ---------
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      double a0[2][2], a1v[2][2];  // [ks][row h] of UX0 (Bx) and UX1 (Dx)
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int ff = g + 8 * h, k = ff >> 1, a1l = ff & 1;
-          const int j = 4 * ks + t;
-          const bool ok = ff < 2 * N && j < N;
-          a0[ks][h] = ok ? UX[ux(c, 0, k, j, 2 * sl + a1l)] : 0.0;
-          a1v[ks][h] = ok ? UX[ux(c, 1, k, j, 2 * sl + a1l)] : 0.0;
-        }
+      const double* ub = UX + c * UX_C + xyf;
       double w0[4] = {0, 0, 0, 0}, w1[4] = {0, 0, 0, 0}, w2[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
-        mma(w0, a1v[ks][0], a1v[ks][1], FB[ks]);  // (Dx, By)
-        mma(w1, a0[ks][0], a0[ks][1], FD[ks]);    // (Bx, Dy)
-        mma(w2, a0[ks][0], a0[ks][1], FB[ks]);    // (Bx, By)
+        const double b0 = ub[yfb[ks][0]], b1 = ub[yfb[ks][1]];                  // UX0 = Bx u
+        const double d0 = ub[UX_V + yfb[ks][0]], d1 = ub[UX_V + yfb[ks][1]];    // UX1 = Dx u
+        mma(w0, d0, d1, FB[ks]);  // (Dx, By)
+        mma(w1, b0, b1, FD[ks]);  // (Bx, Dy)
+        mma(w2, b0, b1, FB[ks]);  // (Bx, By)
       }
+      double* ob = U2 + c * U2_C;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int ff = g + 8 * h, k = ff >> 1, a1l = ff & 1;
-        if (ff < 2 * N) {
-          *reinterpret_cast<double2*>(U2 + u2(c, 0, k, a1l, 2 * t)) = make_double2(w0[2 * h], w0[2 * h + 1]);
-          *reinterpret_cast<double2*>(U2 + u2(c, 1, k, a1l, 2 * t)) = make_double2(w1[2 * h], w1[2 * h + 1]);
-          *reinterpret_cast<double2*>(U2 + u2(c, 2, k, a1l, 2 * t)) = make_double2(w2[2 * h], w2[2 * h + 1]);
+        if (h == 0 || row1) {
+          *reinterpret_cast<double2*>(ob + yfs[h]) = make_double2(w0[2 * h], w0[2 * h + 1]);
+          *reinterpret_cast<double2*>(ob + U2_W + yfs[h]) = make_double2(w1[2 * h], w1[2 * h + 1]);
+          *reinterpret_cast<double2*>(ob + 2 * U2_W + yfs[h]) = make_double2(w2[2 * h], w2[2 * h + 1]);
         }
       }
     }
@@ -247,14 +262,10 @@ __global__ void __launch_bounds__(64 * EPC, 1)
     for (int c = 0; c < 3; ++c)
 #pragma unroll
       for (int w = 0; w < 3; ++w) {
+        const double* ib = U2 + c * U2_C + w * U2_W;
         double acc[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
-          const int k = 4 * ks + t;
-          const double v0 = k < N ? U2[u2(c, w, k, 0, g)] : 0.0;
-          const double v1 = k < N ? U2[u2(c, w, k, 1, g)] : 0.0;
-          mma(acc, v0, v1, w == 2 ? FD[ks] : FB[ks]);
-        }
+        for (int ks = 0; ks < 2; ++ks) mma(acc, ib[zfl[ks][0]], ib[zfl[ks][1]], w == 2 ? FD[ks] : FB[ks]);
 #pragma unroll
         for (int r = 0; r < 4; ++r) G[c][w][r] = acc[r];
       }
@@ -285,10 +296,12 @@ __global__ void __launch_bounds__(64 * EPC, 1)
         mma(v, G[c][d][0], G[c][d][2], d == 2 ? BDp[0] : BBp[0]);
         mma(v, G[c][d][1], G[c][d][3], d == 2 ? BDp[1] : BBp[1]);
         // rows phi (a1l = h, a2 = g), cols k = 2t, 2t+1
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          U2[u2(c, d, 2 * t, h, g)] = v[2 * h];
-          if (2 * t + 1 < N) U2[u2(c, d, 2 * t + 1, h, g)] = v[2 * h + 1];
+        double* ob = U2 + c * U2_C + d * U2_W;
+        ob[zbs[0][0]] = v[0];
+        ob[zbs[0][1]] = v[2];
+        if (t < 3) {
+          ob[zbs[1][0]] = v[1];
+          ob[zbs[1][1]] = v[3];
         }
       }
     __syncwarp();
@@ -296,32 +309,23 @@ __global__ void __launch_bounds__(64 * EPC, 1)
     // ---------------- YB: transposed y -> T0, T1 into UX (this slice's a1 columns) ------
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
+      const double* ib = U2 + c * U2_C;
       double t0[4] = {0, 0, 0, 0}, t1[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
-        double v0[2], v1[2], v2[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int ff = g + 8 * h, k = ff >> 1, a1l = ff & 1;
-          const int a2 = 4 * ks + t;
-          const bool ok = ff < 2 * N;
-          v0[h] = ok ? U2[u2(c, 0, k, a1l, a2)] : 0.0;
-          v1[h] = ok ? U2[u2(c, 1, k, a1l, a2)] : 0.0;
-          v2[h] = ok ? U2[u2(c, 2, k, a1l, a2)] : 0.0;
-        }
-        mma(t0, v0[0], v0[1], BB[ks]);   // By^T V0
-        mma(t1, v1[0], v1[1], BD[ks]);   // Dy^T V1
-        mma(t1, v2[0], v2[1], BB[ks]);   // + By^T V2
+        mma(t0, ib[ybl[ks][0]], ib[ybl[ks][1]], BB[ks]);                    // By^T V0
+        mma(t1, ib[U2_W + ybl[ks][0]], ib[U2_W + ybl[ks][1]], BD[ks]);      // Dy^T V1
+        mma(t1, ib[2 * U2_W + ybl[ks][0]], ib[2 * U2_W + ybl[ks][1]], BB[ks]);  // + By^T V2
       }
+      double* ob = UX + c * UX_C + xyb;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int ff = g + 8 * h, k = ff >> 1, a1l = ff & 1;
-        if (ff < 2 * N) {
-          UX[ux(c, 0, k, 2 * t, 2 * sl + a1l)] = t0[2 * h];
-          UX[ux(c, 1, k, 2 * t, 2 * sl + a1l)] = t1[2 * h];
-          if (2 * t + 1 < N) {
-            UX[ux(c, 0, k, 2 * t + 1, 2 * sl + a1l)] = t0[2 * h + 1];
-            UX[ux(c, 1, k, 2 * t + 1, 2 * sl + a1l)] = t1[2 * h + 1];
+        if (h == 0 || row1) {
+          ob[ybs[0][h]] = t0[2 * h];
+          ob[UX_V + ybs[0][h]] = t1[2 * h];
+          if (t < 3) {
+            ob[ybs[1][h]] = t0[2 * h + 1];
+            ob[UX_V + ybs[1][h]] = t1[2 * h + 1];
           }
         }
       }
@@ -333,12 +337,11 @@ __global__ void __launch_bounds__(64 * EPC, 1)
   // ---------------- XB: transposed x + scatter-add (tiles T = half, half+2, ...) ---------
 #pragma unroll
   for (int u = 0; u < 5; ++u) {
-    const int T = 2 * u + half;
     int cc[2], jj[2], kk[2];
     bool okr[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int f = 16 * T + g + 8 * h;
+      const int f = 16 * (2 * u + half) + g + 8 * h;
       okr[h] = f < 3 * N * N;
       fibre(f, cc[h], jj[h], kk[h]);
     }
@@ -346,24 +349,21 @@ __global__ void __launch_bounds__(64 * EPC, 1)
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
       const int a1 = 4 * ks + t;
-      double p0[2], p1[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        p0[h] = okr[h] ? UX[ux(cc[h], 0, kk[h], jj[h], a1)] : 0.0;
-        p1[h] = okr[h] ? UX[ux(cc[h], 1, kk[h], jj[h], a1)] : 0.0;
-      }
-      mma(o, p0[0], p0[1], BD[ks]);   // Dx^T T0
-      mma(o, p1[0], p1[1], BB[ks]);   // Bx^T T1
+      const double* r0 = UX + cc[0] * UX_C + uxo(kk[0], jj[0], a1);
+      const double* r1 = UX + cc[1] * UX_C + uxo(kk[1], jj[1], a1);
+      mma(o, r0[0], r1[0], BD[ks]);         // Dx^T T0
+      mma(o, r0[UX_V], r1[UX_V], BB[ks]);   // Bx^T T1
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (!okr[h]) continue;
+      double* dst = y + cc[h] * s.nodes + ebase + (int64_t)s.Nx * jj[h] + plane * kk[h];
 #pragma unroll
       for (int uu = 0; uu < 2; ++uu) {
         const int i = 2 * t + uu;
         if (i >= N) continue;
         if (bc && cons(I0 + i, J0 + jj[h], K0 + kk[h], s)) continue;
-        atomicAdd(y + cc[h] * s.nodes + ebase + i + (int64_t)s.Nx * jj[h] + plane * kk[h], o[2 * h + uu]);
+        atomicAdd(dst + i, o[2 * h + uu]);
       }
     }
   }
