@@ -80,6 +80,44 @@ constexpr int pick_S2(int N, int Q) {
   return best;
 }
 
+// element strides of the Z and Y buffers: at low order one warp spans several elements, so
+// pad the element strides to minimise conflicts over whole warps of every stage's pattern
+constexpr int elem_pattern_cost(int N, int Q, int SA, int S2, int ZE, int YE, int NT) {
+  int total = 0;
+  int addr[512] = {0};
+  const int lanes = NT < 512 ? NT : 512;
+  // stage Z / Zt: Z buffer, lanes (i, j, el)
+  for (int w = 0; w < lanes; ++w) addr[w] = (w / (N * N)) * ZE + ((w / N) % N) * N + w % N;
+  total += halfwarp_cost(addr, lanes);
+  // stage Y / Yt: Z buffer and Y buffer, lanes (i, a3, el)
+  for (int w = 0; w < lanes; ++w) addr[w] = (w / (N * Q)) * ZE + ((w / N) % Q) * SA + w % N;
+  total += halfwarp_cost(addr, lanes);
+  for (int w = 0; w < lanes; ++w) addr[w] = (w / (N * Q)) * YE + ((w / N) % Q) * N + w % N;
+  total += halfwarp_cost(addr, lanes);
+  // stage X: Y buffer, lanes (a3, a2, el)
+  for (int w = 0; w < lanes; ++w) addr[w] = (w / (Q * Q)) * YE + ((w / Q) % Q) * S2 + (w % Q) * N;
+  total += halfwarp_cost(addr, lanes);
+  return total;
+}
+
+constexpr int pick_ZE(int N, int Q, int SA, int S2, int ZE0, int YE0, int NT) {
+  int best = ZE0, bc = 1 << 30;
+  for (int p = 0; p < 16; ++p) {
+    const int c = elem_pattern_cost(N, Q, SA, S2, ZE0 + p, YE0, NT);
+    if (c < bc) { bc = c; best = ZE0 + p; }
+  }
+  return best;
+}
+
+constexpr int pick_YE(int N, int Q, int SA, int S2, int ZE, int YE0, int NT) {
+  int best = YE0, bc = 1 << 30;
+  for (int p = 0; p < 16; ++p) {
+    const int c = elem_pattern_cost(N, Q, SA, S2, ZE, YE0 + p, NT);
+    if (c < bc) { bc = c; best = YE0 + p; }
+  }
+  return best;
+}
+
 constexpr int kSmemLimit = 227 * 1024;
 #ifndef ELAS_EB_BY_COLUMNS
 #define ELAS_EB_BY_COLUMNS 0
@@ -106,11 +144,11 @@ struct Cfg {
   static constexpr int SA = pick_SA(N, Q);
   static constexpr int ZV = Q * SA;        // variant stride (Zb | Zd)
   static constexpr int ZC = 2 * ZV;        // component stride
-  static constexpr int ZE = 3 * ZC;        // element stride
+  static constexpr int ZE = pick_ZE(N, Q, SA, pick_S2(N, Q), 3 * ZC, 9 * Q * pick_S2(N, Q), NT);  // element stride
   static constexpr int S2 = pick_S2(N, Q);
   static constexpr int YV = Q * S2;        // variant stride (Y0 | Y1 | Y2)
   static constexpr int YC = 3 * YV;        // component stride
-  static constexpr int YE = 3 * YC;        // element stride
+  static constexpr int YE = pick_YE(N, Q, SA, S2, ZE, 3 * YC, NT);  // element stride
   static constexpr int TAB = 2 * Q * N;    // B then D
   // elements per CTA: enough x-lines for every thread in stage X; at low order also enough
   // z-columns (N^2 per element) to keep every thread busy in stages Z and Zt.
