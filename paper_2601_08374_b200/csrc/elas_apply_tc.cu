@@ -4,7 +4,7 @@
 namespace elas {
 
 cudaError_t apply_tc_info(ApplyLaunch* info) {
-  info->threads = 64 * tc::EPC;
+  info->threads = 32 * tc::WPE * tc::EPC;
   info->elems_per_cta = tc::EPC;
   info->smem_bytes = sizeof(double) * (size_t)tc::EPC * tc::ELEM_SMEM;
   return cudaSuccess;

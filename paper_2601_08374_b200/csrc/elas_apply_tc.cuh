@@ -44,8 +44,18 @@ constexpr int U2_A = 8, U2_K = 2 * U2_A, U2_W = N * U2_K, U2_C = 3 * U2_W, U2_SI
 #ifndef ELAS_TC_EPC
 #define ELAS_TC_EPC 6
 #endif
-constexpr int EPC = ELAS_TC_EPC;               // elements per CTA, two warps each
-constexpr int ELEM_SMEM = UX_SIZE + 2 * U2_SIZE;  // doubles per element (one U2 per warp)
+#ifndef ELAS_TC_WPE
+#define ELAS_TC_WPE 2
+#endif
+#ifndef ELAS_TC_AQ_EARLY
+#define ELAS_TC_AQ_EARLY 1
+#endif
+constexpr int EPC = ELAS_TC_EPC;               // elements per CTA
+constexpr int WPE = ELAS_TC_WPE;               // warps per element (2 or 4): slices split between them
+constexpr int ELEM_SMEM = UX_SIZE + WPE * U2_SIZE;  // doubles per element (one U2 per warp)
+constexpr int XTILES = (3 * N * N + 15) / 16;       // 10 fibre tiles in the x stages
+constexpr int XT_PER_WARP = (XTILES + WPE - 1) / WPE;
+static_assert(NSLICE % WPE == 0, "slices must split evenly over the warps of an element");
 constexpr int QD_PER_ELEM = 9 * Q * Q * Q;     // 4608 doubles, fragment order (see qdata kernel)
 
 // swizzled offsets inside one (c, v) block of UX / one (c, w) block of U2
@@ -91,9 +101,9 @@ __device__ __forceinline__ void pointwise(double (&G)[3][3], const double* A, do
       G[c][d] = fma(S[c][2], A[3 * d + 2], fma(S[c][1], A[3 * d + 1], S[c][0] * A[3 * d]));
 }
 
-// Named barrier for the two warps of element `el` (ids 1..EPC; 0 is __syncthreads).
+// Named barrier for the WPE warps of element `el` (ids 1..EPC; 0 is __syncthreads).
 __device__ __forceinline__ void pair_sync(int el) {
-  asm volatile("bar.sync %0, 64;" ::"r"(el + 1) : "memory");
+  asm volatile("bar.sync %0, %1;" ::"r"(el + 1), "r"(32 * WPE) : "memory");
 }
 
 // fibre f of the x stages -> (c, j, k), f = c*49 + k*7 + j; rows past the last fibre are
@@ -106,13 +116,13 @@ __device__ __forceinline__ void fibre(int f, int& c, int& j, int& k) {
   j = r - k * N;
 }
 
-__global__ void __launch_bounds__(64 * EPC, 1)
+__global__ void __launch_bounds__(32 * WPE * EPC, 1)
     apply_tc_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
                     const double* __restrict__ rr, const double* __restrict__ tables, Slab s,
                     int64_t e_begin, int64_t e_end, int pref_ctas) {
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int el = warp >> 1, half = warp & 1;
+  const int el = warp / WPE, half = warp % WPE;   // `half`: this warp's index within its element
   const int g = lane >> 2, t = lane & 3;
   const int64_t cta_e0 = e_begin + (int64_t)blockIdx.x * EPC;
   const int64_t e = cta_e0 + el;
@@ -158,13 +168,13 @@ __global__ void __launch_bounds__(64 * EPC, 1)
 
   // ---------------- XF: gather + contraction in x (tiles T = half, half+2, ...) ----------
   {
-    double a[5][2][2];  // all gathers of this warp issued before any MMA
+    double a[XT_PER_WARP][2][2];  // all gathers of this warp issued before any MMA
 #pragma unroll
-    for (int u = 0; u < 5; ++u)
+    for (int u = 0; u < XT_PER_WARP; ++u)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         int c, j, k;
-        fibre(16 * (2 * u + half) + g + 8 * h, c, j, k);
+        fibre(16 * (WPE * u + half) + g + 8 * h, c, j, k);
         const double* src = x + c * s.nodes + ebase + (int64_t)s.Nx * j + plane * k;
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
@@ -173,7 +183,8 @@ __global__ void __launch_bounds__(64 * EPC, 1)
         }
       }
 #pragma unroll
-    for (int u = 0; u < 5; ++u) {
+    for (int u = 0; u < XT_PER_WARP; ++u) {
+      if (WPE * u + half >= XTILES) break;
       double cb[4] = {0, 0, 0, 0}, cd[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
@@ -182,7 +193,7 @@ __global__ void __launch_bounds__(64 * EPC, 1)
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int f = 16 * (2 * u + half) + g + 8 * h;
+        const int f = 16 * (WPE * u + half) + g + 8 * h;
         int c, j, k;
         fibre(f, c, j, k);
         double* dst = UX + c * UX_C + uxo(k, j, 2 * t);
@@ -219,16 +230,18 @@ __global__ void __launch_bounds__(64 * EPC, 1)
   const double* qe = qd + e * (int64_t)QD_PER_ELEM;
 
 #pragma unroll 1
-  for (int ss = 0; ss < 2; ++ss) {
-    const int sl = 2 * half + ss;   // this warp's slices: a1 in {2 sl, 2 sl + 1}
+  for (int ss = 0; ss < NSLICE / WPE; ++ss) {
+    const int sl = (NSLICE / WPE) * half + ss;   // this warp's slices: a1 in {2 sl, 2 sl + 1}
     const int xyf = (2 * sl) ^ sw_yf, xyb = (2 * sl) ^ sw_yb;
-    // qdata of this slice: 4 points x 9 values per lane, issued early (consumed after ZF)
-    double Aq[4][9];
+    // qdata of this slice: 4 points x 9 values per lane (issued early unless register-starved)
     const double* qs = qe + sl * 4 * 9 * 32 + lane;
+#if ELAS_TC_AQ_EARLY
+    double Aq[4][9];
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int f = 0; f < 9; ++f) Aq[r][f] = __ldg(qs + (r * 9 + f) * 32);
+#endif
 
     // ---------------- YF: contraction in y (fibres ff = 2k + a1l, 14 of 16 rows) ---------
 #pragma unroll
@@ -278,7 +291,14 @@ __global__ void __launch_bounds__(64 * EPC, 1)
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int d = 0; d < 3; ++d) Gp[c][d] = G[c][d][r];
+#if ELAS_TC_AQ_EARLY
       pointwise(Gp, Aq[r], re);
+#else
+      double Ar[9];
+#pragma unroll
+      for (int f = 0; f < 9; ++f) Ar[f] = __ldg(qs + (r * 9 + f) * 32);
+      pointwise(Gp, Ar, re);
+#endif
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -336,12 +356,13 @@ __global__ void __launch_bounds__(64 * EPC, 1)
 
   // ---------------- XB: transposed x + scatter-add (tiles T = half, half+2, ...) ---------
 #pragma unroll
-  for (int u = 0; u < 5; ++u) {
+  for (int u = 0; u < XT_PER_WARP; ++u) {
+    if (WPE * u + half >= XTILES) break;
     int cc[2], jj[2], kk[2];
     bool okr[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int f = 16 * (2 * u + half) + g + 8 * h;
+      const int f = 16 * (WPE * u + half) + g + 8 * h;
       okr[h] = f < 3 * N * N;
       fibre(f, cc[h], jj[h], kk[h]);
     }
