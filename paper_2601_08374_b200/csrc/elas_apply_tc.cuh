@@ -244,44 +244,69 @@ __global__ void __launch_bounds__(32 * WPE * EPC, 1)
 #endif
 
     // ---------------- YF: contraction in y (fibres ff = 2k + a1l, 14 of 16 rows) ---------
+    {
+      double bx[3][2][2], dx[3][2][2];  // [c][ks][h]: UX0 = Bx u, UX1 = Dx u
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double* ub = UX + c * UX_C + xyf;
-      double w0[4] = {0, 0, 0, 0}, w1[4] = {0, 0, 0, 0}, w2[4] = {0, 0, 0, 0};
+      for (int c = 0; c < 3; ++c)
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const double b0 = ub[yfb[ks][0]], b1 = ub[yfb[ks][1]];                  // UX0 = Bx u
-        const double d0 = ub[UX_V + yfb[ks][0]], d1 = ub[UX_V + yfb[ks][1]];    // UX1 = Dx u
-        mma(w0, d0, d1, FB[ks]);  // (Dx, By)
-        mma(w1, b0, b1, FD[ks]);  // (Bx, Dy)
-        mma(w2, b0, b1, FB[ks]);  // (Bx, By)
-      }
-      double* ob = U2 + c * U2_C;
+        for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (h == 0 || row1) {
-          *reinterpret_cast<double2*>(ob + yfs[h]) = make_double2(w0[2 * h], w0[2 * h + 1]);
-          *reinterpret_cast<double2*>(ob + U2_W + yfs[h]) = make_double2(w1[2 * h], w1[2 * h + 1]);
-          *reinterpret_cast<double2*>(ob + 2 * U2_W + yfs[h]) = make_double2(w2[2 * h], w2[2 * h + 1]);
+          for (int h = 0; h < 2; ++h) {
+            bx[c][ks][h] = UX[c * UX_C + xyf + yfb[ks][h]];
+            dx[c][ks][h] = UX[c * UX_C + UX_V + xyf + yfb[ks][h]];
+          }
+      double w[3][3][4];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int v = 0; v < 3; ++v)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) w[c][v][r] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          mma(w[c][0], dx[c][ks][0], dx[c][ks][1], FB[ks]);  // (Dx, By)
+          mma(w[c][1], bx[c][ks][0], bx[c][ks][1], FD[ks]);  // (Bx, Dy)
+          mma(w[c][2], bx[c][ks][0], bx[c][ks][1], FB[ks]);  // (Bx, By)
         }
-      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+          double* ob = U2 + c * U2_C + v * U2_W;
+          *reinterpret_cast<double2*>(ob + yfs[0]) = make_double2(w[c][v][0], w[c][v][1]);
+          if (row1) *reinterpret_cast<double2*>(ob + yfs[1]) = make_double2(w[c][v][2], w[c][v][3]);
+        }
     }
     __syncwarp();
 
     // ---------------- ZF: contraction in z -> gradients in C fragments -----------------
     // rows: phi = g -> (a1l 0, a2 g), phi = g+8 -> (a1l 1, a2 g); cols a3 = 2t, 2t+1
     double G[3][3][4];
+    {
+      double zi[3][3][2][2];  // [c][w][ks][h]
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
+      for (int c = 0; c < 3; ++c)
 #pragma unroll
-      for (int w = 0; w < 3; ++w) {
-        const double* ib = U2 + c * U2_C + w * U2_W;
-        double acc[4] = {0, 0, 0, 0};
+        for (int w = 0; w < 3; ++w)
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) mma(acc, ib[zfl[ks][0]], ib[zfl[ks][1]], w == 2 ? FD[ks] : FB[ks]);
+          for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) G[c][w][r] = acc[r];
-      }
+            for (int h = 0; h < 2; ++h) zi[c][w][ks][h] = U2[c * U2_C + w * U2_W + zfl[ks][h]];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int w = 0; w < 3; ++w)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) G[c][w][r] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int w = 0; w < 3; ++w) mma(G[c][w], zi[c][w][ks][0], zi[c][w][ks][1], w == 2 ? FD[ks] : FB[ks]);
+    }
 
     // ---------------- pointwise on the fragments -------------------------------------
 #pragma unroll
@@ -308,44 +333,76 @@ __global__ void __launch_bounds__(32 * WPE * EPC, 1)
 
     // ---------------- ZB: transposed z, A operand straight from the C fragments ---------
     // K position (ks, t) <-> a3 = 2t + ks: ks = 0 uses c0/c2, ks = 1 uses c1/c3
+    {
+      double v[3][3][4];
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
+      for (int c = 0; c < 3; ++c)
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        double v[4] = {0, 0, 0, 0};
-        mma(v, G[c][d][0], G[c][d][2], d == 2 ? BDp[0] : BBp[0]);
-        mma(v, G[c][d][1], G[c][d][3], d == 2 ? BDp[1] : BBp[1]);
-        // rows phi (a1l = h, a2 = g), cols k = 2t, 2t+1
-        double* ob = U2 + c * U2_C + d * U2_W;
-        ob[zbs[0][0]] = v[0];
-        ob[zbs[0][1]] = v[2];
-        if (t < 3) {
-          ob[zbs[1][0]] = v[1];
-          ob[zbs[1][1]] = v[3];
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) v[c][d][r] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+            mma(v[c][d], G[c][d][ks], G[c][d][2 + ks], d == 2 ? BDp[ks] : BBp[ks]);
+      // rows phi (a1l = h, a2 = g), cols k = 2t, 2t+1
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          double* ob = U2 + c * U2_C + d * U2_W;
+          ob[zbs[0][0]] = v[c][d][0];
+          ob[zbs[0][1]] = v[c][d][2];
+          if (t < 3) {
+            ob[zbs[1][0]] = v[c][d][1];
+            ob[zbs[1][1]] = v[c][d][3];
+          }
         }
-      }
+    }
     __syncwarp();
 
     // ---------------- YB: transposed y -> T0, T1 into UX (this slice's a1 columns) ------
+    {
+      double vi[3][3][2][2];  // [c][d][ks][h]
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double* ib = U2 + c * U2_C;
-      double t0[4] = {0, 0, 0, 0}, t1[4] = {0, 0, 0, 0};
+      for (int c = 0; c < 3; ++c)
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        mma(t0, ib[ybl[ks][0]], ib[ybl[ks][1]], BB[ks]);                    // By^T V0
-        mma(t1, ib[U2_W + ybl[ks][0]], ib[U2_W + ybl[ks][1]], BD[ks]);      // Dy^T V1
-        mma(t1, ib[2 * U2_W + ybl[ks][0]], ib[2 * U2_W + ybl[ks][1]], BB[ks]);  // + By^T V2
-      }
-      double* ob = UX + c * UX_C + xyb;
+        for (int d = 0; d < 3; ++d)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (h == 0 || row1) {
-          ob[ybs[0][h]] = t0[2 * h];
-          ob[UX_V + ybs[0][h]] = t1[2 * h];
-          if (t < 3) {
-            ob[ybs[1][h]] = t0[2 * h + 1];
-            ob[UX_V + ybs[1][h]] = t1[2 * h + 1];
+          for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) vi[c][d][ks][h] = U2[c * U2_C + d * U2_W + ybl[ks][h]];
+      double t0[3][4], t1[3][4];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) t0[c][r] = t1[c][r] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          mma(t0[c], vi[c][0][ks][0], vi[c][0][ks][1], BB[ks]);   // By^T V0
+          mma(t1[c], vi[c][1][ks][0], vi[c][1][ks][1], BD[ks]);   // Dy^T V1
+        }
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) mma(t1[c], vi[c][2][ks][0], vi[c][2][ks][1], BB[ks]);  // + By^T V2
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double* ob = UX + c * UX_C + xyb;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 0 || row1) {
+            ob[ybs[0][h]] = t0[c][2 * h];
+            ob[UX_V + ybs[0][h]] = t1[c][2 * h];
+            if (t < 3) {
+              ob[ybs[1][h]] = t0[c][2 * h + 1];
+              ob[UX_V + ybs[1][h]] = t1[c][2 * h + 1];
+            }
           }
         }
       }
