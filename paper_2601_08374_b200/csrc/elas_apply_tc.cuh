@@ -72,6 +72,13 @@ __device__ __forceinline__ void mma(double (&c)[4], double a0, double a1, double
       : "d"(a0), "d"(a1), "d"(b));
 }
 
+// 8-row variant (SASS: one DMMA.8x8x4): a0 = A[g][t], b0 = B[t][g], c0/c1 = C[g][2t], C[g][2t+1]
+__device__ __forceinline__ void mma8(double (&c)[2], double a0, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a0), "d"(b));
+}
+
 __device__ __forceinline__ bool cons(int I, int J, int K, const Slab& s) {
   const uint32_t f = s.faces;
   return ((f & ELAS_FACE_XMIN) && I == 0) || ((f & ELAS_FACE_XMAX) && I == s.Nx - 1) ||
@@ -166,6 +173,19 @@ __global__ void __launch_bounds__(32 * WPE * EPC, 1)
   const int64_t ebase = I0 + (int64_t)s.Nx * J0 + plane * K0;
   const int iK[2] = {t, (4 + t) < N ? 4 + t : N - 1};   // K index 4 ks + t, clamped (zero coefficient)
 
+  const double* qe = qd + e * (int64_t)QD_PER_ELEM;
+#if ELAS_TC_AQ_EARLY == 2
+  // the first slice's qdata is requested before the x stage so its latency hides behind it
+  double Aq[4][9];
+  {
+    const double* qs = qe + (NSLICE / WPE) * half * 4 * 9 * 32 + lane;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int f = 0; f < 9; ++f) Aq[r][f] = __ldg(qs + (r * 9 + f) * 32);
+  }
+#endif
+
   // ---------------- XF: gather + contraction in x (tiles T = half, half+2, ...) ----------
   {
     double a[XT_PER_WARP][2][2];  // all gathers of this warp issued before any MMA
@@ -227,21 +247,18 @@ __global__ void __launch_bounds__(32 * WPE * EPC, 1)
   pair_sync(el);
 
   const double re = __ldg(rr + e);
-  const double* qe = qd + e * (int64_t)QD_PER_ELEM;
 
 #pragma unroll 1
   for (int ss = 0; ss < NSLICE / WPE; ++ss) {
     const int sl = (NSLICE / WPE) * half + ss;   // this warp's slices: a1 in {2 sl, 2 sl + 1}
     const int xyf = (2 * sl) ^ sw_yf, xyb = (2 * sl) ^ sw_yb;
-    // qdata of this slice: 4 points x 9 values per lane (issued early unless register-starved)
-    const double* qs = qe + sl * 4 * 9 * 32 + lane;
-#if ELAS_TC_AQ_EARLY
-    double Aq[4][9];
+    const double* qs = qe + sl * 4 * 9 * 32 + lane;   // qdata of this slice, fragment order
+    // rows h = 0 of the fused z stage: qdata of points r = 0, 1 requested before the y stage
+    double Aq[2][9];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < 2; ++r)
 #pragma unroll
       for (int f = 0; f < 9; ++f) Aq[r][f] = __ldg(qs + (r * 9 + f) * 32);
-#endif
 
     // ---------------- YF: contraction in y (fibres ff = 2k + a1l, 14 of 16 rows) ---------
     {
@@ -281,85 +298,78 @@ __global__ void __launch_bounds__(32 * WPE * EPC, 1)
     }
     __syncwarp();
 
-    // ---------------- ZF: contraction in z -> gradients in C fragments -----------------
-    // rows: phi = g -> (a1l 0, a2 g), phi = g+8 -> (a1l 1, a2 g); cols a3 = 2t, 2t+1
-    double G[3][3][4];
-    {
-      double zi[3][3][2][2];  // [c][w][ks][h]
+    // ---------------- fused z stage, one 8-row half (a1l = h) at a time ---------------
+    // ZF: rows phi = g -> (a1l = h, a2 = g); cols a3 = 2t, 2t+1  -> gradients G[c][d][2]
+    // pointwise on the two points (a1l = h, a2 = g, a3 = 2t + u), qdata r = 2h + u
+    // ZB: K position (ks, t) <-> a3 = 2t + ks, A operand straight from G; rows -> U2 rows
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double G[3][3][2];
+      {
+        double zi[3][3][2];  // [c][w][ks]
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int w = 0; w < 3; ++w)
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) zi[c][w][ks] = U2[c * U2_C + w * U2_W + zfl[ks][h]];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int w = 0; w < 3; ++w) G[c][w][0] = G[c][w][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int w = 0; w < 3; ++w) mma8(G[c][w], zi[c][w][ks], w == 2 ? FD[ks] : FB[ks]);
+      }
+      double An[2][9];   // qdata of the other half, requested now (consumed next iteration)
+      if (h == 0) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int f = 0; f < 9; ++f) An[r][f] = __ldg(qs + ((2 + r) * 9 + f) * 32);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        double Gp[3][3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) Gp[c][d] = G[c][d][u];
+        pointwise(Gp, Aq[u], re);
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) G[c][d][u] = Gp[c][d];
+      }
+      if (h == 0) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int f = 0; f < 9; ++f) Aq[r][f] = An[r][f];
+      }
+      __syncwarp();  // every lane has read its ZF inputs of rows h before they are overwritten
+      double v[3][3][2];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int w = 0; w < 3; ++w)
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) zi[c][w][ks][h] = U2[c * U2_C + w * U2_W + zfl[ks][h]];
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int w = 0; w < 3; ++w)
-#pragma unroll
-          for (int r = 0; r < 4; ++r) G[c][w][r] = 0.0;
+        for (int d = 0; d < 3; ++d) v[c][d][0] = v[c][d][1] = 0.0;
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
-          for (int w = 0; w < 3; ++w) mma(G[c][w], zi[c][w][ks][0], zi[c][w][ks][1], w == 2 ? FD[ks] : FB[ks]);
-    }
-
-    // ---------------- pointwise on the fragments -------------------------------------
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      double Gp[3][3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) Gp[c][d] = G[c][d][r];
-#if ELAS_TC_AQ_EARLY
-      pointwise(Gp, Aq[r], re);
-#else
-      double Ar[9];
-#pragma unroll
-      for (int f = 0; f < 9; ++f) Ar[f] = __ldg(qs + (r * 9 + f) * 32);
-      pointwise(Gp, Ar, re);
-#endif
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) G[c][d][r] = Gp[c][d];
-    }
-    __syncwarp();  // all lanes finished reading U2 before it is overwritten
-
-    // ---------------- ZB: transposed z, A operand straight from the C fragments ---------
-    // K position (ks, t) <-> a3 = 2t + ks: ks = 0 uses c0/c2, ks = 1 uses c1/c3
-    {
-      double v[3][3][4];
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int d = 0; d < 3; ++d)
-#pragma unroll
-          for (int r = 0; r < 4; ++r) v[c][d][r] = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int d = 0; d < 3; ++d)
-            mma(v[c][d], G[c][d][ks], G[c][d][2 + ks], d == 2 ? BDp[ks] : BBp[ks]);
-      // rows phi (a1l = h, a2 = g), cols k = 2t, 2t+1
+          for (int d = 0; d < 3; ++d) mma8(v[c][d], G[c][d][ks], d == 2 ? BDp[ks] : BBp[ks]);
+      // rows (a1l = h, a2 = g), cols k = 2t, 2t+1
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           double* ob = U2 + c * U2_C + d * U2_W;
-          ob[zbs[0][0]] = v[c][d][0];
-          ob[zbs[0][1]] = v[c][d][2];
-          if (t < 3) {
-            ob[zbs[1][0]] = v[c][d][1];
-            ob[zbs[1][1]] = v[c][d][3];
-          }
+          ob[zbs[0][h]] = v[c][d][0];
+          if (t < 3) ob[zbs[1][h]] = v[c][d][1];
         }
     }
     __syncwarp();
