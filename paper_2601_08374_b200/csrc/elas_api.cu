@@ -17,6 +17,10 @@
 #define ELAS_AUTO_TENSOR 1
 #endif
 static constexpr bool kAutoTensor = ELAS_AUTO_TENSOR != 0;
+#ifndef ELAS_AUTO_THREAD
+#define ELAS_AUTO_THREAD 1
+#endif
+static constexpr bool kAutoThread = ELAS_AUTO_THREAD != 0;
 
 namespace elas {
 
@@ -197,8 +201,10 @@ int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* m
     cudaFree(dbad);
   };
   cudaError_t e;
-  const int qlayout = op->variant == ELAS_VARIANT_TENSOR ? elas::QD_LAYOUT_TC6 : elas::QD_LAYOUT_LINES;
-  const size_t qbytes = sizeof(double) * (size_t)elas::qd_stride(q, qlayout) * (size_t)ne;
+  const int qlayout = op->variant == ELAS_VARIANT_TENSOR   ? elas::QD_LAYOUT_TC6
+                      : op->variant == ELAS_VARIANT_THREAD ? elas::QD_LAYOUT_E32
+                                                           : elas::QD_LAYOUT_LINES;
+  const size_t qbytes = sizeof(double) * (size_t)elas::qd_stride(q, qlayout) * (size_t)elas::qd_elems(ne, qlayout);
   if ((e = cudaMalloc(&op->qd, qbytes)) != cudaSuccess ||
       (e = cudaMalloc(&op->rr, sizeof(double) * ne)) != cudaSuccess ||
       (e = cudaMalloc(&op->tab, sizeof(double) * tabh.size())) != cudaSuccess ||
@@ -254,6 +260,8 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
   }
   cudaError_t e = op->variant == ELAS_VARIANT_TENSOR
                       ? elas::apply_tc_launch(op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
+                  : op->variant == ELAS_VARIANT_THREAD
+                      ? elas::apply_p1t_launch(op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
                       : elas::apply_launch(op->p, op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st);
   if (e != cudaSuccess) return cuda_fail(e, "apply kernel launch");
   if (op->prof) CUDA_OR(cudaEventRecord(ev1, st), "cudaEventRecord");
@@ -299,13 +307,18 @@ elas_op* elas_create(const elas_mesh* m, int p, int q, const double* lambda, con
 
 elas_op* elas_create_ex(const elas_mesh* m, int p, int q, const double* lambda, const double* mu, int variant) {
   elas::g_err.clear();
-  if (variant < ELAS_VARIANT_AUTO || variant > ELAS_VARIANT_TENSOR) {
+  if (variant < ELAS_VARIANT_AUTO || variant > ELAS_VARIANT_THREAD) {
     set_error("elas_create_ex: unknown variant");
     return nullptr;
   }
   const bool tc_ok = (p == 6 && q == 8);
+  const bool thread_ok = (p == 1);
   if (variant == ELAS_VARIANT_TENSOR && !tc_ok) {
     set_error("elas_create_ex: the tensor-core variant exists for p = 6, q = 8 only");
+    return nullptr;
+  }
+  if (variant == ELAS_VARIANT_THREAD && !thread_ok) {
+    set_error("elas_create_ex: the one-thread-per-element variant exists for p = 1 only");
     return nullptr;
   }
   if (!m || !lambda || !mu) { set_error("elas_create: NULL mesh/lambda/mu"); return nullptr; }
@@ -327,7 +340,9 @@ elas_op* elas_create_ex(const elas_mesh* m, int p, int q, const double* lambda, 
   elas_op* op = new elas_op();
   op->p = p;
   op->q = q;
-  op->variant = (variant == ELAS_VARIANT_AUTO) ? (tc_ok && kAutoTensor ? ELAS_VARIANT_TENSOR : ELAS_VARIANT_SIMT) : variant;
+  if (variant == ELAS_VARIANT_AUTO)
+    variant = (tc_ok && kAutoTensor) ? ELAS_VARIANT_TENSOR : (thread_ok && kAutoThread) ? ELAS_VARIANT_THREAD : ELAS_VARIANT_SIMT;
+  op->variant = variant;
   op->nranks = m->nranks < 1 ? 1 : m->nranks;
   op->rank = m->rank;
   int32_t b, e;

@@ -41,12 +41,20 @@ cudaError_t apply_tc_launch(const Slab& s, const double* x, double* y, const dou
 
 // qdata layouts: 0 = qd[e][a1][f][a3 + q a2] (SIMT kernel), 1 = fragment order of the tensor-core
 // kernel: qd[e][slice a1/2][r][f][lane], r = 2 (a1 % 2) + a3 % 2, lane = 4 a2 + a3 / 2.
-enum { QD_LAYOUT_LINES = 0, QD_LAYOUT_TC6 = 1 };
+// 2 = lane-interleaved blocks of 32 elements for the one-thread-per-element p = 1 kernel:
+//     qd[e / 32][pt][f][e % 32], pt = a1 + q (a2 + q a3).
+enum { QD_LAYOUT_LINES = 0, QD_LAYOUT_TC6 = 1, QD_LAYOUT_E32 = 2 };
 
 // qdata doubles per element: 9 q^3 rounded up to even so every element starts 16-B aligned
 // (TMA bulk copies need 16-B aligned addresses and sizes).
 constexpr int qd_stride_lines(int q) { return (9 * q * q * q + 1) & ~1; }
-inline int qd_stride(int q, int layout) { return layout == QD_LAYOUT_TC6 ? 9 * q * q * q : qd_stride_lines(q); }
+inline int qd_stride(int q, int layout) { return layout == QD_LAYOUT_LINES ? qd_stride_lines(q) : 9 * q * q * q; }
+// elements the qdata allocation must cover (E32 pads to whole blocks of 32)
+inline int64_t qd_elems(int64_t ne, int layout) { return layout == QD_LAYOUT_E32 ? (ne + 31) / 32 * 32 : ne; }
+
+// one-thread-per-element kernel, p = 1 (elas_apply_p1t.cu)
+cudaError_t apply_p1t_launch(int q, const Slab& s, const double* x, double* y, const double* qd, const double* rr,
+                             const double* tables, int64_t e_begin, int64_t e_end, cudaStream_t st);
 
 // Kernels in elas_setup.cu
 cudaError_t launch_qdata(int p, int q, int layout, const Slab& s, const double* verts, const double* lam,

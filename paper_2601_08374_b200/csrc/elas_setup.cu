@@ -71,7 +71,11 @@ __global__ void qdata_kernel(int q, int layout, Slab s, const double* __restrict
     }
     const double W = qp.w[a1] * qp.w[a2] * qp.w[a3] * det;
     const double sc = sqrt(mu[e] * W) / det;   // A~ = sqrt(mu W) J^{-1} = sqrt(mu W) adj / det
-    if (layout == QD_LAYOUT_TC6) {
+    if (layout == QD_LAYOUT_E32) {
+      double* out = qd + (e >> 5) * (int64_t)(32 * 9 * q3) + (int64_t)pt * 9 * 32 + (e & 31);
+      for (int d = 0; d < 3; ++d)
+        for (int m = 0; m < 3; ++m) out[(3 * d + m) * 32] = sc * adj[d][m];
+    } else if (layout == QD_LAYOUT_TC6) {
       // fragment order of apply_tc_kernel (q = 8): 32 lanes contiguous per (slice, r, f)
       const int sl = a1 >> 1, r = 2 * (a1 & 1) + (a3 & 1), lane = 4 * a2 + (a3 >> 1);
       double* out = qd + e * (int64_t)(9 * q3) + (int64_t)((sl * 4 + r) * 9) * 32 + lane;

@@ -17,7 +17,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", os.environ.get("ELAS_LIBNAME", "libelas.so"))
 
-VARIANT_AUTO, VARIANT_SIMT, VARIANT_TENSOR = 0, 1, 2
+VARIANT_AUTO, VARIANT_SIMT, VARIANT_TENSOR, VARIANT_THREAD = 0, 1, 2, 3
 ELAS_OK, ELAS_EINVAL, ELAS_EGEOM, ELAS_ENOMEM, ELAS_ECUDA, ELAS_ENCCL = 0, -1, -2, -3, -4, -5
 FACE_XMIN, FACE_XMAX, FACE_YMIN, FACE_YMAX, FACE_ZMIN, FACE_ZMAX = 1, 2, 4, 8, 16, 32
 

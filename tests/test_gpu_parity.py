@@ -340,3 +340,19 @@ def test_tensor_variant_only_for_p6_q8():
     h = elas.elas_create_ex(2, 2, 2, 6, 7, 1.0, 1.0)
     assert elas.elas_variant(h) == elas.VARIANT_SIMT
     elas.elas_destroy(h)
+
+
+@pytest.mark.parametrize("variant", [1, 3])
+@pytest.mark.parametrize("q", [2, 3])
+@pytest.mark.parametrize("dims,faces", [((5, 3, 4), 1 | 8 | 16), ((33, 2, 3), 63), ((1, 1, 1), 0), ((70, 1, 1), 2)])
+def test_p1_variants_vs_oracle(variant, q, dims, faces):
+    """p = 1: the one-thread-per-element kernel (and the fibre kernel) vs the oracle; element
+    counts straddle the 32-element qdata blocks and the 128-thread CTAs."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_problem("t", *dims, 1, q, perturb=True, lognormal_material=True, faces=faces, seed=60 + q)
+    op = Operator.from_problem(P, variant=variant)
+    assert op.variant == variant
+    y = gpu_apply(P, op=op)
+    op.close()
+    assert rel_l2(y, oracle.apply(oracle_mesh(P), P.x)) <= TOL
