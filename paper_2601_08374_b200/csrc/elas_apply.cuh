@@ -195,8 +195,29 @@ __device__ __forceinline__ void pointwise(double (&g)[3][3], const double (&A)[9
       g[c][d] = fma(S[c][2], A[3 * d + 2], fma(S[c][1], A[3 * d + 1], S[c][0] * A[3 * d]));
 }
 
+// CTAs per SM the register allocation targets (ELAS_MINB_P<p>, default 1 = up to 255 regs)
+#ifndef ELAS_MINB_P4
+#define ELAS_MINB_P4 3   // measured: p = 4 at 3 CTAs/SM (168 regs) 20.8 -> 21.3 GDoF/s
+#endif
+#ifndef ELAS_MINB_DEFAULT
+#define ELAS_MINB_DEFAULT 1
+#endif
+template <int P> struct MinBlocks { static constexpr int value = ELAS_MINB_DEFAULT; };
+#ifdef ELAS_MINB_P2
+template <> struct MinBlocks<2> { static constexpr int value = ELAS_MINB_P2; };
+#endif
+#ifdef ELAS_MINB_P3
+template <> struct MinBlocks<3> { static constexpr int value = ELAS_MINB_P3; };
+#endif
+#ifdef ELAS_MINB_P4
+template <> struct MinBlocks<4> { static constexpr int value = ELAS_MINB_P4; };
+#endif
+#ifdef ELAS_MINB_P5
+template <> struct MinBlocks<5> { static constexpr int value = ELAS_MINB_P5; };
+#endif
+
 template <int P, int Q>
-__global__ void __launch_bounds__(Cfg<P, Q>::NT, 1)
+__global__ void __launch_bounds__(Cfg<P, Q>::NT, MinBlocks<P>::value)
     apply_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
                  const double* __restrict__ rr, const double* __restrict__ tables, Slab s,
                  int64_t e_begin, int64_t e_end, int pref_ctas) {

@@ -47,6 +47,9 @@ constexpr int U2_A = 8, U2_K = 2 * U2_A, U2_W = N * U2_K, U2_C = 3 * U2_W, U2_SI
 #ifndef ELAS_TC_WPE
 #define ELAS_TC_WPE 2
 #endif
+#ifndef ELAS_TC_PF
+#define ELAS_TC_PF 1
+#endif
 #ifndef ELAS_TC_AQ_EARLY
 #define ELAS_TC_AQ_EARLY 1
 #endif
@@ -134,9 +137,10 @@ __global__ void __launch_bounds__(32 * WPE * EPC, 1)
   const int64_t cta_e0 = e_begin + (int64_t)blockIdx.x * EPC;
   const int64_t e = cta_e0 + el;
 #if ELAS_L2_PREFETCH
+  // TMA bulk prefetch of quadrature data into L2 (ELAS_TC_PF: 1 = the CTA one wave ahead,
+  // 2 = this CTA's own elements at CTA start, 3 = 2 + each warp's next slice)
   if (threadIdx.x == 0 && pref_ctas > 0) {
-    // TMA bulk prefetch into L2 of the qdata of the CTA one wave ahead
-    const int64_t pe0 = cta_e0 + (int64_t)pref_ctas * EPC;
+    const int64_t pe0 = (ELAS_TC_PF == 1) ? cta_e0 + (int64_t)pref_ctas * EPC : cta_e0;
     if (pe0 < e_end) {
       const int64_t pne = (e_end - pe0) < EPC ? (e_end - pe0) : EPC;
       const uintptr_t a0 = (uintptr_t)(qd + pe0 * (int64_t)QD_PER_ELEM);
@@ -253,6 +257,11 @@ __global__ void __launch_bounds__(32 * WPE * EPC, 1)
     const int sl = (NSLICE / WPE) * half + ss;   // this warp's slices: a1 in {2 sl, 2 sl + 1}
     const int xyf = (2 * sl) ^ sw_yf, xyb = (2 * sl) ^ sw_yb;
     const double* qs = qe + sl * 4 * 9 * 32 + lane;   // qdata of this slice, fragment order
+#if ELAS_L2_PREFETCH
+    if (ELAS_TC_PF == 3 && lane == 0 && ss + 1 < NSLICE / WPE)   // the warp's next slice -> L2
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qe + (sl + 1) * 4 * 9 * 32),
+                   "r"((uint32_t)(4 * 9 * 32 * 8)) : "memory");
+#endif
     // rows h = 0 of the fused z stage: qdata of points r = 0, 1 requested before the y stage
     double Aq[2][9];
 #pragma unroll
