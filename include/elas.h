@@ -88,19 +88,22 @@ elas_op* elas_create(const elas_mesh* mesh, int p, int q, const double* lambda, 
  *   ELAS_VARIANT_TENSOR FP64 tensor cores (mma.sync f64 / DMMA), one warp per element
  *                       (p = 6, q = 8 only);
  *   ELAS_VARIANT_THREAD one thread per element, sum factorisation in registers (p = 1 only);
+ *   ELAS_VARIANT_FOLDED the SIMT kernel with even-odd folded 1D contractions (every p, q;
+ *                       half the sum-factorisation FMAs; same qdata layout as SIMT);
  *   ELAS_VARIANT_AUTO   the faster measured variant for (p, q).
  * The choice fixes the quadrature-data layout, so it is made at creation. */
 #define ELAS_VARIANT_AUTO 0
 #define ELAS_VARIANT_SIMT 1
 #define ELAS_VARIANT_TENSOR 2
 #define ELAS_VARIANT_THREAD 3
+#define ELAS_VARIANT_FOLDED 4
 
 /* elas_create with an explicit kernel variant; NULL + ELAS_EINVAL message if the variant
  * does not exist for (p, q). */
 elas_op* elas_create_ex(const elas_mesh* mesh, int p, int q, const double* lambda, const double* mu,
                         int variant);
 
-/* The resolved variant of an op (ELAS_VARIANT_SIMT, _TENSOR or _THREAD), -1 if NULL. */
+/* The resolved variant of an op (ELAS_VARIANT_SIMT, _TENSOR, _THREAD or _FOLDED), -1 if NULL. */
 int elas_variant(const elas_op* op);
 
 /* y = A x (overwrite), or y = Z A Z x + (I - Z) x with Dirichlet faces.

@@ -21,6 +21,12 @@ static constexpr bool kAutoTensor = ELAS_AUTO_TENSOR != 0;
 #define ELAS_AUTO_THREAD 1
 #endif
 static constexpr bool kAutoThread = ELAS_AUTO_THREAD != 0;
+// measured (tools/ab_variants.py, config 4): the folded kernel beats the plain SIMT kernel at
+// every p = 2..8 (+5 % at p = 2, +19 % p = 4, +52 % p = 8)
+#ifndef ELAS_AUTO_FOLDED
+#define ELAS_AUTO_FOLDED 1
+#endif
+static constexpr bool kAutoFolded = ELAS_AUTO_FOLDED != 0;
 
 namespace elas {
 
@@ -35,6 +41,13 @@ thread_local std::string g_err;
   cudaError_t apply_launch_p##P(int q, const Slab& s, const double* x, double* y, const double* qd, \
                                 const double* rr, const double* tables, int64_t e_begin,        \
                                 int64_t e_end, cudaStream_t st);
+DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
+#undef DECL
+#define DECL(P)                                                                                  \
+  cudaError_t apply_eo_info_p##P(int q, ApplyLaunch* info);                                      \
+  cudaError_t apply_eo_launch_p##P(int q, const Slab& s, const double* x, double* y, const double* qd, \
+                                   const double* rr, const double* tables, int64_t e_begin,     \
+                                   int64_t e_end, cudaStream_t st);
 DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
 #undef DECL
 
@@ -59,6 +72,26 @@ cudaError_t apply_launch(int p, int q, const Slab& s, const double* x, double* y
                          cudaStream_t st) {
   switch (p) {
 #define CASE(P) case P: return apply_launch_p##P(q, s, x, y, qd, rr, tables, e_begin, e_end, st);
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t apply_eo_info(int p, int q, ApplyLaunch* info) {
+  switch (p) {
+#define CASE(P) case P: return apply_eo_info_p##P(q, info);
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t apply_eo_launch(int p, int q, const Slab& s, const double* x, double* y, const double* qd,
+                            const double* rr, const double* tables, int64_t e_begin, int64_t e_end,
+                            cudaStream_t st) {
+  switch (p) {
+#define CASE(P) case P: return apply_eo_launch_p##P(q, s, x, y, qd, rr, tables, e_begin, e_end, st);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
     default: return cudaErrorInvalidValue;
@@ -189,8 +222,12 @@ int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* m
   }
   // 1D tables
   const int n = p + 1;
-  std::vector<double> g(q), w(q), tabh(2 * q * n);
+  // tables = B | D | fold(B) | fold(D)  (the folded copies feed ELAS_VARIANT_FOLDED)
+  const int fts = elas::fold_table_size(p, q);
+  std::vector<double> g(q), w(q), tabh(2 * q * n + 2 * fts);
   elas::host_tables(p, q, nullptr, g.data(), w.data(), tabh.data(), tabh.data() + q * n);
+  elas::host_fold_table(p, q, tabh.data(), tabh.data() + 2 * q * n);
+  elas::host_fold_table(p, q, tabh.data() + q * n, tabh.data() + 2 * q * n + fts);
 
   double *dV = nullptr, *dlam = nullptr, *dmu = nullptr;
   int* dbad = nullptr;
@@ -262,6 +299,8 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
                       ? elas::apply_tc_launch(op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
                   : op->variant == ELAS_VARIANT_THREAD
                       ? elas::apply_p1t_launch(op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
+                  : op->variant == ELAS_VARIANT_FOLDED
+                      ? elas::apply_eo_launch(op->p, op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
                       : elas::apply_launch(op->p, op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st);
   if (e != cudaSuccess) return cuda_fail(e, "apply kernel launch");
   if (op->prof) CUDA_OR(cudaEventRecord(ev1, st), "cudaEventRecord");
@@ -307,7 +346,7 @@ elas_op* elas_create(const elas_mesh* m, int p, int q, const double* lambda, con
 
 elas_op* elas_create_ex(const elas_mesh* m, int p, int q, const double* lambda, const double* mu, int variant) {
   elas::g_err.clear();
-  if (variant < ELAS_VARIANT_AUTO || variant > ELAS_VARIANT_THREAD) {
+  if (variant < ELAS_VARIANT_AUTO || variant > ELAS_VARIANT_FOLDED) {
     set_error("elas_create_ex: unknown variant");
     return nullptr;
   }
@@ -341,7 +380,10 @@ elas_op* elas_create_ex(const elas_mesh* m, int p, int q, const double* lambda, 
   op->p = p;
   op->q = q;
   if (variant == ELAS_VARIANT_AUTO)
-    variant = (tc_ok && kAutoTensor) ? ELAS_VARIANT_TENSOR : (thread_ok && kAutoThread) ? ELAS_VARIANT_THREAD : ELAS_VARIANT_SIMT;
+    variant = (tc_ok && kAutoTensor)       ? ELAS_VARIANT_TENSOR
+              : (thread_ok && kAutoThread) ? ELAS_VARIANT_THREAD
+              : kAutoFolded                ? ELAS_VARIANT_FOLDED
+                                           : ELAS_VARIANT_SIMT;
   op->variant = variant;
   op->nranks = m->nranks < 1 ? 1 : m->nranks;
   op->rank = m->rank;

@@ -137,7 +137,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 #define ELAS_NT 128
 #endif
 
-template <int P, int Q>
+template <int P, int Q, int TABSZ = 2 * Q * (P + 1)>
 struct Cfg {
   static constexpr int N = P + 1;
   static constexpr int NT = ELAS_NT;
@@ -149,7 +149,7 @@ struct Cfg {
   static constexpr int YV = Q * S2;        // variant stride (Y0 | Y1 | Y2)
   static constexpr int YC = 3 * YV;        // component stride
   static constexpr int YE = pick_YE(N, Q, SA, S2, ZE, 3 * YC, NT);  // element stride
-  static constexpr int TAB = 2 * Q * N;    // B then D
+  static constexpr int TAB = (TABSZ + 1) & ~1;  // coefficient tables (B then D, or folded)
   // elements per CTA: enough x-lines for every thread in stage X; at low order also enough
   // z-columns (N^2 per element) to keep every thread busy in stages Z and Zt.
   static constexpr int EB_lines = (NT / (Q * Q)) > 0 ? NT / (Q * Q) : 1;

@@ -26,6 +26,15 @@ struct ApplyLaunch {
 
 // Host tables (elas_tables.cpp): GLL nodes, Gauss-Legendre rule, barycentric Lagrange.
 int host_tables(int p, int q, double* nodes, double* points, double* weights, double* B, double* D);
+// Even-odd folded copy of one table (elas_tables.cpp); op tables = B | D | fold(B) | fold(D).
+int fold_table_size(int p, int q);
+void host_fold_table(int p, int q, const double* T, double* out);
+
+// folded-SIMT variant (elas_apply_eo_p<P>.cu)
+cudaError_t apply_eo_info(int p, int q, ApplyLaunch* info);
+cudaError_t apply_eo_launch(int p, int q, const Slab& s, const double* x, double* y, const double* qd,
+                            const double* rr, const double* tables, int64_t e_begin, int64_t e_end,
+                            cudaStream_t st);
 
 // Per-degree translation units (elas_apply_p<P>.cu) export these; q must be p+1 or p+2.
 // Returns cudaSuccess or an error; `info` only queries the configuration.

@@ -145,4 +145,36 @@ int host_tables(int p, int q, double* nodes, double* points, double* weights, do
   return ELAS_OK;
 }
 
+// Even-odd folded form of one q x n table T (B: parity +1, D: parity -1), DESIGN.md section 6.
+// GLL nodes and Gauss points are symmetric about 1/2, so T[q-1-a][n-1-i] = s T[a][i].  With
+// u+_i = u_i + u_{n-1-i}, u-_i = u_i - u_{n-1-i} (i < n/2) the forward contraction is
+//   E_a = sum_i FE[a][i] u+_i (+ FE[a][n/2] u_mid),  O_a = sum_i FO[a][i] u-_i,
+//   (T u)_a = E_a + O_a,  (T u)_{q-1-a} = s (E_a - O_a)                 (a < (q+1)/2)
+// and the transposed one the same with the roles of points and nodes swapped (BE, BO).
+// Layout (fold_table_size doubles): FE[qe][ne] | FO[qe][nh] | BE[ne][qe] | BO[ne][qh],
+// ne = (n+1)/2, nh = n/2, qe = (q+1)/2, qh = q/2.
+int fold_table_size(int p, int q) { return ((q + 1) / 2) * (p + 1) + ((p + 2) / 2) * q; }
+
+void host_fold_table(int p, int q, const double* T, double* out) {
+  const int n = p + 1, ne = (n + 1) / 2, nh = n / 2, qe = (q + 1) / 2, qh = q / 2;
+  double* FE = out;
+  double* FO = FE + qe * ne;
+  double* BE = FE + qe * n;
+  double* BO = BE + ne * qe;
+  for (int a = 0; a < qe; ++a) {
+    for (int i = 0; i < nh; ++i) {
+      FE[a * ne + i] = 0.5 * (T[a * n + i] + T[a * n + n - 1 - i]);
+      FO[a * nh + i] = 0.5 * (T[a * n + i] - T[a * n + n - 1 - i]);
+    }
+    if (n & 1) FE[a * ne + nh] = T[a * n + nh];
+  }
+  for (int j = 0; j < ne; ++j) {
+    for (int a = 0; a < qh; ++a) {
+      BE[j * qe + a] = 0.5 * (T[a * n + j] + T[(q - 1 - a) * n + j]);
+      BO[j * qh + a] = 0.5 * (T[a * n + j] - T[(q - 1 - a) * n + j]);
+    }
+    if (q & 1) BE[j * qe + qh] = T[qh * n + j];
+  }
+}
+
 }  // namespace elas

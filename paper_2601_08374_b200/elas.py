@@ -17,7 +17,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", os.environ.get("ELAS_LIBNAME", "libelas.so"))
 
-VARIANT_AUTO, VARIANT_SIMT, VARIANT_TENSOR, VARIANT_THREAD = 0, 1, 2, 3
+VARIANT_AUTO, VARIANT_SIMT, VARIANT_TENSOR, VARIANT_THREAD, VARIANT_FOLDED = 0, 1, 2, 3, 4
 ELAS_OK, ELAS_EINVAL, ELAS_EGEOM, ELAS_ENOMEM, ELAS_ECUDA, ELAS_ENCCL = 0, -1, -2, -3, -4, -5
 FACE_XMIN, FACE_XMAX, FACE_YMIN, FACE_YMAX, FACE_ZMIN, FACE_ZMAX = 1, 2, 4, 8, 16, 32
 
@@ -157,7 +157,7 @@ def elas_variant(h):
 
 def elas_create_ex(nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0), faces=0,
                    rank=0, nranks=1, nccl_id=None, variant=VARIANT_AUTO):
-    """elas_create with an explicit kernel variant (VARIANT_AUTO / _SIMT / _TENSOR)."""
+    """elas_create with an explicit kernel variant (VARIANT_AUTO / _SIMT / _TENSOR / _THREAD / _FOLDED)."""
     lib = load()
     lam_a = np.ascontiguousarray(np.asarray(lam, dtype=np.float64).reshape(-1))
     mu_a = np.ascontiguousarray(np.asarray(mu, dtype=np.float64).reshape(-1))

@@ -338,7 +338,7 @@ def test_tensor_variant_only_for_p6_q8():
     assert elas.elas_variant(h) == elas.VARIANT_TENSOR
     elas.elas_destroy(h)
     h = elas.elas_create_ex(2, 2, 2, 6, 7, 1.0, 1.0)
-    assert elas.elas_variant(h) == elas.VARIANT_SIMT
+    assert elas.elas_variant(h) == elas.VARIANT_FOLDED
     elas.elas_destroy(h)
 
 
@@ -356,3 +356,37 @@ def test_p1_variants_vs_oracle(variant, q, dims, faces):
     y = gpu_apply(P, op=op)
     op.close()
     assert rel_l2(y, oracle.apply(oracle_mesh(P), P.x)) <= TOL
+
+
+# ---------------------------------------------------------------------------------------
+# folded SIMT variant (even-odd folded 1D contractions), every p and both q
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("p", range(1, 9))
+@pytest.mark.parametrize("dq", [1, 2])
+@pytest.mark.parametrize("dims,faces", [((3, 2, 3), 1 | 8 | 16), ((1, 1, 1), 0), ((5, 4, 3), 63 ^ 16)])
+def test_folded_variant_vs_oracle(p, dq, dims, faces):
+    """Odd and even n and q (mid rows/columns of the folded tables), Dirichlet faces on both
+    ends of a fold (nodes i and n-1-i), ragged element counts."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator, VARIANT_FOLDED
+    P = synth.make_problem("t", *dims, p, p + dq, perturb=True, lognormal_material=True, faces=faces,
+                           seed=200 + 10 * p + dq)
+    op = Operator.from_problem(P, variant=VARIANT_FOLDED)
+    assert op.variant == VARIANT_FOLDED
+    y = gpu_apply(P, op=op)
+    op.close()
+    assert rel_l2(y, oracle.apply(oracle_mesh(P), P.x)) <= TOL
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_folded_agrees_with_simt(cfg):
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator, VARIANT_SIMT, VARIANT_FOLDED
+    P = synth.make_config(cfg)
+    ys = []
+    for variant in (VARIANT_SIMT, VARIANT_FOLDED):
+        op = Operator.from_problem(P, variant=variant)
+        ys.append(gpu_apply(P, op=op))
+        op.close()
+    assert rel_l2(ys[1], ys[0]) <= 1e-14
