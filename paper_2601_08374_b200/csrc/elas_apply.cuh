@@ -137,10 +137,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 #define ELAS_NT 128
 #endif
 
-template <int P, int Q, int TABSZ = 2 * Q * (P + 1)>
+template <int P, int Q, int TABSZ = 2 * Q * (P + 1), int NTHR = ELAS_NT>
 struct Cfg {
   static constexpr int N = P + 1;
-  static constexpr int NT = ELAS_NT;
+  static constexpr int NT = NTHR;
   static constexpr int SA = pick_SA(N, Q);
   static constexpr int ZV = Q * SA;        // variant stride (Zb | Zd)
   static constexpr int ZC = 2 * ZV;        // component stride

@@ -31,8 +31,94 @@ struct Fold {
   static constexpr int QHX = QH > 0 ? QH : 1;
 };
 
+// CTA size and register target of the folded kernel per degree (ELAS_EO_NT_P<p>,
+// ELAS_EO_MINB_P<p> override; measured by tools/ab_libs.sh)
+template <int P> struct NtEO { static constexpr int value = ELAS_NT; };
+template <int P> struct MinbEO { static constexpr int value = P == 2 ? 4 : MinBlocks<P>::value; };
+#ifdef ELAS_EO_NT_P2
+template <> struct NtEO<2> { static constexpr int value = ELAS_EO_NT_P2; };
+#endif
+#ifdef ELAS_EO_NT_P3
+template <> struct NtEO<3> { static constexpr int value = ELAS_EO_NT_P3; };
+#endif
+#ifdef ELAS_EO_NT_P4
+template <> struct NtEO<4> { static constexpr int value = ELAS_EO_NT_P4; };
+#endif
+#ifdef ELAS_EO_NT_P5
+template <> struct NtEO<5> { static constexpr int value = ELAS_EO_NT_P5; };
+#endif
+#ifdef ELAS_EO_NT_P6
+template <> struct NtEO<6> { static constexpr int value = ELAS_EO_NT_P6; };
+#endif
+#ifdef ELAS_EO_NT_P7
+template <> struct NtEO<7> { static constexpr int value = ELAS_EO_NT_P7; };
+#endif
+#ifdef ELAS_EO_NT_P8
+template <> struct NtEO<8> { static constexpr int value = ELAS_EO_NT_P8; };
+#endif
+#ifdef ELAS_EO_MINB_P2
+template <> struct MinbEO<2> { static constexpr int value = ELAS_EO_MINB_P2; };
+#endif
+#ifdef ELAS_EO_MINB_P3
+template <> struct MinbEO<3> { static constexpr int value = ELAS_EO_MINB_P3; };
+#endif
+#ifdef ELAS_EO_MINB_P4
+template <> struct MinbEO<4> { static constexpr int value = ELAS_EO_MINB_P4; };
+#endif
+#ifdef ELAS_EO_MINB_P5
+template <> struct MinbEO<5> { static constexpr int value = ELAS_EO_MINB_P5; };
+#endif
+#ifdef ELAS_EO_MINB_P6
+template <> struct MinbEO<6> { static constexpr int value = ELAS_EO_MINB_P6; };
+#endif
+#ifdef ELAS_EO_MINB_P7
+template <> struct MinbEO<7> { static constexpr int value = ELAS_EO_MINB_P7; };
+#endif
+#ifdef ELAS_EO_MINB_P8
+template <> struct MinbEO<8> { static constexpr int value = ELAS_EO_MINB_P8; };
+#endif
+
 template <int P, int Q>
-using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS>;
+using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEO<P>::value>;
+
+// Quadrature-data ring (ELAS_QD_RING = R > 0): every stage-X thread owns one x-line (EB q^2 <=
+// NT), so it streams ITS line's 9 values per point into its own shared-memory slots with
+// cp.async (LDGSTS, no registers, no CTA barrier), R-1 points ahead of the pointwise stage; the
+// first R-1 points are requested at CTA start and land during stages Z and Y.  Slots are
+// [R][9][NT] so both the copies and the reads are contiguous across a warp.
+// measured (tools/ab_libs.sh, config 4): an aliased ring of 4 points helps at p >= 6
+// (p6 29.9 -> 30.7, p8 27.5 -> 28.8 GDoF/s); at p <= 5 the Z buffer holds at most 2 slots per
+// thread and the one-point register prefetch is as good or better.
+#ifndef ELAS_QD_RING
+#define ELAS_QD_RING (P >= 6 ? 4 : 0)
+#endif
+// whole-CTA TMA staging of qdata where two CTAs fit (elas_apply.cuh); off at p = 2, which
+// runs faster at 4 CTAs/SM without it (12.5 -> 16 GDoF/s)
+template <int P> struct StageEO { static constexpr bool value = P != 2; };
+#ifndef ELAS_QD_RING_ALIAS
+#define ELAS_QD_RING_ALIAS 1
+#endif
+template <int P, int Q>
+struct RingEO {
+  using C = CfgEO<P, Q>;
+  // ALIAS: the ring lives in the Z buffer, idle during stage X (first copies issued after the
+  // stage-Y barrier); otherwise it gets its own shared memory and starts at CTA begin.
+  static constexpr bool ALIAS = ELAS_QD_RING_ALIAS != 0;
+  static constexpr int RMAX = ALIAS ? (C::EB * C::ZE) / (9 * C::NT) : 16;
+  static constexpr int R0 = ELAS_QD_RING < RMAX ? ELAS_QD_RING : RMAX;
+  static constexpr int R = R0 >= 2 ? R0 : 0;
+  static constexpr bool STAGE = C::STAGE_QD && R == 0 && StageEO<P>::value;  // whole-CTA TMA staging
+  static constexpr int OFF = ALIAS ? C::TAB : (C::TAB + C::EB * (C::ZE + C::YE) + 1) & ~1;
+  static constexpr size_t smem = (R > 0 && !ALIAS) ? 8u * (size_t)(OFF + R * 9 * C::NT)
+                                 : STAGE ? C::smem : 8u * (size_t)(C::TAB + C::EB * (C::ZE + C::YE));
+};
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // u (n values per component) -> even (ne) / odd (nh) halves
 template <int N, int NE, int NHX>
@@ -49,7 +135,7 @@ __device__ __forceinline__ void fold_in(const double (&u)[3][N], double (&up)[3]
 }
 
 template <int P, int Q>
-__global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinBlocks<P>::value)
+__global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
     apply_eo_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
                     const double* __restrict__ rr, const double* __restrict__ tables, Slab s,
                     int64_t e_begin, int64_t e_end, int pref_ctas) {
@@ -57,6 +143,8 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinBlocks<P>::value)
   using F = Fold<P, Q>;
   constexpr int N = C::N, NT = C::NT, EB = C::EB;
   constexpr int NE = F::NE, NH = F::NH, QE = F::QE, QH = F::QH, NHX = F::NHX;
+  using RG = RingEO<P, Q>;
+  constexpr int R = RG::R;
   extern __shared__ double smem[];
   double* tB = smem;            // folded B (parity +1)
   double* tD = smem + F::TS;    // folded D (parity -1)
@@ -68,7 +156,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinBlocks<P>::value)
   const int tid = threadIdx.x;
   const int64_t e0 = e_begin + (int64_t)blockIdx.x * EB;
   const int ne = (int)((e_end - e0) < EB ? (e_end - e0) : EB);
-  if constexpr (C::STAGE_QD) {
+  if constexpr (RG::STAGE) {
     if (tid == 0) {
       const uint32_t bar = smem_u32(mbar);
       const uint32_t bytes = (uint32_t)(8 * ne * C::QDE);
@@ -80,6 +168,21 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinBlocks<P>::value)
           "l"(qd + e0 * (int64_t)C::QDE), "r"(bytes), "r"(bar)
           : "memory");
     }
+  }
+  // this thread's stage-X line (at most one: EB q^2 <= NT) and its qdata ring
+  double* ring = smem + RG::OFF + tid;
+  const bool has_line = tid < ne * Q * Q;
+  const double* qline = qd + (e0 + tid / (Q * Q)) * (int64_t)C::QDE + tid % (Q * Q);
+  auto ring_issue = [&](int a1) {
+    if (has_line) {
+#pragma unroll
+      for (int f = 0; f < 9; ++f) cp_async8(ring + ((a1 % (R > 0 ? R : 1)) * 9 + f) * NT, qline + (a1 * 9 + f) * Q * Q);
+    }
+    cp_async_commit();
+  };
+  if constexpr (R > 0 && !RG::ALIAS) {
+#pragma unroll
+    for (int a1 = 0; a1 < R - 1; ++a1) ring_issue(a1);
   }
   {
     const double* ft = tables + 2 * Q * N;   // fold(B) | fold(D) follow the plain tables
@@ -225,7 +328,11 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinBlocks<P>::value)
   __syncthreads();
 
   // ---------------- Stage X + pointwise + transposed X (folded) -------------------------
-  if constexpr (C::STAGE_QD) {
+  if constexpr (R > 0 && RG::ALIAS) {   // the Z buffer is free now
+#pragma unroll
+    for (int a1 = 0; a1 < R - 1; ++a1) ring_issue(a1);
+  }
+  if constexpr (RG::STAGE) {
     const uint32_t bar = smem_u32(mbar);
     asm volatile(
         "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(bar)
@@ -278,18 +385,28 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinBlocks<P>::value)
       }
     }
     const double r = __ldg(rr + e);
-    const double* qp = C::STAGE_QD ? sQ + el * C::QDE + L : qd + e * (int64_t)C::QDE + L;
+    const double* qp = RG::STAGE ? sQ + el * C::QDE + L : qd + e * (int64_t)C::QDE + L;
     double An[9];
+    if constexpr (R == 0) {
 #pragma unroll
-    for (int f = 0; f < 9; ++f) An[f] = qp[f * Q * Q];
+      for (int f = 0; f < 9; ++f) An[f] = qp[f * Q * Q];
+    }
 #pragma unroll
     for (int a1 = 0; a1 < Q; ++a1) {
       double A[9];
+      if constexpr (R > 0) {
+        if (a1 + R - 1 < Q) ring_issue(a1 + R - 1);
+        else cp_async_commit();                    // empty group keeps the count uniform
+        cp_async_wait<R - 1>();                    // this thread's copies of point a1 landed
 #pragma unroll
-      for (int f = 0; f < 9; ++f) A[f] = An[f];
-      if (a1 + 1 < Q) {
+        for (int f = 0; f < 9; ++f) A[f] = ring[((a1 % R) * 9 + f) * NT];
+      } else {
 #pragma unroll
-        for (int f = 0; f < 9; ++f) An[f] = qp[((a1 + 1) * 9 + f) * Q * Q];
+        for (int f = 0; f < 9; ++f) A[f] = An[f];
+        if (a1 + 1 < Q) {
+#pragma unroll
+          for (int f = 0; f < 9; ++f) An[f] = qp[((a1 + 1) * 9 + f) * Q * Q];
+        }
       }
       double G[3][3];
 #pragma unroll
@@ -490,19 +607,19 @@ cudaError_t launch_apply_eo_pq(const Slab& s, const double* x, double* y, const 
   static int pref = -1;
   if (!attr_done) {
     cudaError_t err = cudaFuncSetAttribute(apply_eo_kernel<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)C::smem);
+                                           (int)RingEO<P, Q>::smem);
     if (err != cudaSuccess) return err;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_eo_kernel<P, Q>, C::NT, C::smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_eo_kernel<P, Q>, C::NT, RingEO<P, Q>::smem);
     pref = sms * (per_sm > 0 ? per_sm : 1);
     attr_done = true;
   }
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
   const int64_t grid = (ne + C::EB - 1) / C::EB;
-  apply_eo_kernel<P, Q><<<(unsigned)grid, C::NT, C::smem, st>>>(x, y, qd, rr, tables, s, e_begin, e_end, pref);
+  apply_eo_kernel<P, Q><<<(unsigned)grid, C::NT, RingEO<P, Q>::smem, st>>>(x, y, qd, rr, tables, s, e_begin, e_end, pref);
   return cudaGetLastError();
 }
 
@@ -511,7 +628,7 @@ void info_eo_pq(ApplyLaunch* info) {
   using C = CfgEO<P, Q>;
   info->threads = C::NT;
   info->elems_per_cta = C::EB;
-  info->smem_bytes = C::smem;
+  info->smem_bytes = RingEO<P, Q>::smem;
 }
 
 }  // namespace elas
