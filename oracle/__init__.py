@@ -37,3 +37,4 @@ from .elasticity import (  # noqa: F401
     constrained_mask,
     node_coordinates,
 )
+from .solvers import diagonal, power_lambda_max, chebyshev, pcg  # noqa: F401

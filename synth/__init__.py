@@ -156,3 +156,20 @@ def make_config(cfg, p=None, draw_x=True):
         return make_problem("cfg5", 64, 64, 256, 6, 8, lengths=(1.0, 1.0, 4.0), perturb=True,
                             lognormal_material=True, seed=4, draw_x=draw_x)
     raise ValueError(f"unknown config {cfg}")
+
+
+def splitmix_uniform(n, seed):
+    """Counter-based draw in [-1, 1): u_i = 2 * (splitmix64(seed, i) >> 11) * 2^-53 - 1.
+
+    splitmix64(seed, i): z = seed + (i + 1) * 0x9E3779B97F4A7C15 (mod 2^64);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9; z = (z ^ (z >> 27)) * 0x94D049BB133111EB;
+    z ^= z >> 31.  The power-iteration start vector (reading R19); libelas implements
+    the same counter-based generator for its default start vector.
+    """
+    with np.errstate(over="ignore"):
+        i = np.arange(1, n + 1, dtype=np.uint64)
+        z = np.uint64(seed) + i * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return 2.0 * (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53) - 1.0
