@@ -149,6 +149,54 @@ int elas_launches_per_apply(const elas_op* op);
 int elas_profile(elas_op* op, int enable);
 int elas_profile_read(elas_op* op, double* apply_kernel_ms, int64_t* launches);
 
+/* Solver layer: the consumers of the apply in the paper's solver (
+ * PAPER.md:202-210 Sec. 3.1 "Chebyshev polynomial smoother ... the action of the matrix
+ * operator A and an estimate of the operator's spectral radius ... a few Lanczos or power
+ * iterations"; PAPER.md:164 CG).  Readings R18-R21 in DESIGN.md.  All vectors are DEVICE
+ * pointers of elas_local_dofs(op) doubles, 8-byte aligned, on the op's stream. ----------- */
+
+/* d = diag(Z A Z + (I - Z)): the diagonal of the operator elas_apply applies (constrained
+ * rows 1), by a sum-factorised setup kernel (one CTA per element, 6 x 3 contracted q^3
+ * tensors).  Multi-GPU: as elas_apply (NCCL mode sums the interface planes; external mode
+ * leaves partial planes for elas_interface_add).  ELAS_OK / ELAS_EINVAL / ELAS_ECUDA. */
+int elas_diagonal(elas_op* op, double* d);
+
+/* Chebyshev smoother on D^{-1} A (D = elas_diagonal), single-GPU operators (nranks == 1).
+ * Create: computes and caches D^{-1} in the op, runs `power_iters` power iterations
+ *   v <- v/|v|; w = D^{-1} A v; lam = v.w; v <- w/|w|
+ * from v0 (DEVICE, NULL => splitmix64 counter generator with `seed`, the same generator as
+ * synth.splitmix_uniform) and sets lam_max = 1.1 lam.  The polynomial is the degree-`order`
+ * Chebyshev polynomial for the interval [alpha lam_max, beta lam_max] (SPEC defaults 3, 0.1,
+ * 1.1).  NULL + ELAS_EINVAL message on bad arguments (order < 1, !(0 < alpha < beta),
+ * power_iters < 1, nranks > 1) or a non-positive estimate.  Owns 3 work vectors. */
+typedef struct elas_cheb elas_cheb;
+elas_cheb* elas_cheb_create(elas_op* op, int order, double alpha, double beta, int power_iters, const double* v0,
+                            unsigned long long seed);
+/* 1.1 x the power-iteration estimate (-1 if NULL). */
+double elas_cheb_lambda_max(const elas_cheb* ch);
+/* One smoothing pass: x <- x + p_k(D^{-1} A) D^{-1} (b - A x), classical three-term Chebyshev
+ * iteration (order applies of the operator).  b, x must not alias.  Asynchronous. */
+int elas_cheb_apply(elas_cheb* ch, const double* b, double* x);
+void elas_cheb_destroy(elas_cheb* ch);   /* NULL-safe; synchronises the op's stream */
+
+/* Preconditioned conjugate gradients from x = 0 (single-GPU operators).  precond:
+ * ELAS_PC_NONE, ELAS_PC_JACOBI (D^{-1}, cached in the op) or ELAS_PC_CHEBYSHEV (z =
+ * p_k(D^{-1}A) D^{-1} r, `cheb` of the same op).  Stops when sqrt(r.z / r0.z0) <= rtol or after
+ * maxit iterations (not an error: report.converged = 0).  history (HOST, maxit + 1 doubles or
+ * NULL) receives sqrt(r_i.z_i / r0.z0).  Synchronises once per iteration (8-byte read of r.z).
+ * Dots are deterministic (fixed two-pass reduction order).  ELAS_OK / ELAS_EINVAL (bad
+ * arguments, preconditioner not positive) / ELAS_ECUDA. */
+#define ELAS_PC_NONE 0
+#define ELAS_PC_JACOBI 1
+#define ELAS_PC_CHEBYSHEV 2
+typedef struct {
+  int iterations;       /* iterations performed                                         */
+  int converged;        /* 1 if rel_residual <= rtol                                    */
+  double rel_residual;  /* sqrt(r.z / r0.z0) at exit                                     */
+} elas_solve_report;
+int elas_pcg(elas_op* op, int precond, elas_cheb* cheb, const double* b, double* x, double rtol, int maxit,
+             elas_solve_report* report, double* history);
+
 /* Thread-local message describing the last error on this thread ("" if none). */
 const char* elas_last_error(void);
 

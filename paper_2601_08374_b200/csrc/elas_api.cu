@@ -8,7 +8,7 @@
 #include <string>
 #include <vector>
 
-#include "elas_internal.h"
+#include "elas_op.h"
 
 #define ELAS_VERSION 10000
 
@@ -103,30 +103,6 @@ cudaError_t apply_eo_launch(int p, int q, const Slab& s, const double* x, double
 using elas::Slab;
 using elas::set_error;
 
-struct elas_op {
-  int p = 0, q = 0, rank = 0, nranks = 1;
-  int variant = ELAS_VARIANT_SIMT;  // resolved kernel variant
-  int32_t ez0 = 0, ez1 = 0;
-  Slab slab{};
-  int device = 0;
-  bool external = false;            // nranks > 1 without a communicator
-  double* qd = nullptr;             // 9 q^3 doubles per element
-  double* rr = nullptr;             // lambda/mu per element
-  double* tab = nullptr;            // B then D (q x (p+1) each)
-  double* xs = nullptr;             // staging for elas_apply_host
-  double* ys = nullptr;
-  cudaStream_t stream = nullptr;
-  // multi-GPU
-  ncclComm_t comm = nullptr;
-  cudaStream_t comm_stream = nullptr;
-  cudaEvent_t ev_boundary = nullptr, ev_comm = nullptr;
-  double* halo_lo = nullptr;
-  double* halo_hi = nullptr;
-  // measurement hook
-  bool prof = false;
-  std::vector<cudaEvent_t> prof_ev;   // pairs (start, stop), reused
-  size_t prof_used = 0;
-};
 
 namespace {
 
@@ -166,6 +142,7 @@ void free_op(elas_op* op) {
   if (op->ev_boundary) cudaEventDestroy(op->ev_boundary);
   if (op->ev_comm) cudaEventDestroy(op->ev_comm);
   for (cudaEvent_t ev : op->prof_ev) cudaEventDestroy(ev);
+  elas::free_solver_state(op);
   delete op;
 }
 
@@ -241,6 +218,7 @@ int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* m
   const int qlayout = op->variant == ELAS_VARIANT_TENSOR   ? elas::QD_LAYOUT_TC6
                       : op->variant == ELAS_VARIANT_THREAD ? elas::QD_LAYOUT_E32
                                                            : elas::QD_LAYOUT_LINES;
+  op->qlayout = qlayout;
   const size_t qbytes = sizeof(double) * (size_t)elas::qd_stride(q, qlayout) * (size_t)elas::qd_elems(ne, qlayout);
   if ((e = cudaMalloc(&op->qd, qbytes)) != cudaSuccess ||
       (e = cudaMalloc(&op->rr, sizeof(double) * ne)) != cudaSuccess ||
@@ -308,6 +286,38 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
 }
 
 }  // namespace
+
+namespace elas {
+
+int exchange_planes(elas_op* op, double* y) {
+  if (op->nranks == 1 || op->external) return ELAS_OK;
+  const Slab& s = op->slab;
+  cudaStream_t st = op->stream;
+  const bool lo = op->rank > 0, hi = op->rank < op->nranks - 1;
+  const int64_t plane = (int64_t)s.Nx * s.Ny;
+  CUDA_OR(cudaEventRecord(op->ev_boundary, st), "cudaEventRecord");
+  CUDA_OR(cudaStreamWaitEvent(op->comm_stream, op->ev_boundary, 0), "cudaStreamWaitEvent");
+  NCCL_OR(ncclGroupStart(), "ncclGroupStart");
+  for (int c = 0; c < 3; ++c) {
+    if (lo) {
+      NCCL_OR(ncclSend(y + c * s.nodes, plane, ncclDouble, op->rank - 1, op->comm, op->comm_stream), "ncclSend");
+      NCCL_OR(ncclRecv(op->halo_lo + c * plane, plane, ncclDouble, op->rank - 1, op->comm, op->comm_stream), "ncclRecv");
+    }
+    if (hi) {
+      NCCL_OR(ncclSend(y + c * s.nodes + (int64_t)(s.Nz - 1) * plane, plane, ncclDouble, op->rank + 1, op->comm,
+                       op->comm_stream), "ncclSend");
+      NCCL_OR(ncclRecv(op->halo_hi + c * plane, plane, ncclDouble, op->rank + 1, op->comm, op->comm_stream), "ncclRecv");
+    }
+  }
+  NCCL_OR(ncclGroupEnd(), "ncclGroupEnd");
+  CUDA_OR(cudaEventRecord(op->ev_comm, op->comm_stream), "cudaEventRecord");
+  CUDA_OR(cudaStreamWaitEvent(st, op->ev_comm, 0), "cudaStreamWaitEvent");
+  if (lo) CUDA_OR(launch_plane_add(s, 0, y, op->halo_lo, st), "plane add launch");
+  if (hi) CUDA_OR(launch_plane_add(s, s.Nz - 1, y, op->halo_hi, st), "plane add launch");
+  return ELAS_OK;
+}
+
+}  // namespace elas
 
 extern "C" {
 

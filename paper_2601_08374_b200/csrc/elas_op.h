@@ -1,0 +1,46 @@
+// The operator object behind the opaque elas_op handle (shared by elas_api.cu and
+// elas_solver.cu; not part of the public ABI).
+#pragma once
+#include <nccl.h>
+
+#include <vector>
+
+#include "elas_internal.h"
+
+struct elas_op {
+  int p = 0, q = 0, rank = 0, nranks = 1;
+  int variant = ELAS_VARIANT_SIMT;  // resolved kernel variant
+  int32_t ez0 = 0, ez1 = 0;
+  elas::Slab slab{};
+  int device = 0;
+  bool external = false;            // nranks > 1 without a communicator
+  double* qd = nullptr;             // 9 q^3 doubles per element
+  double* rr = nullptr;             // lambda/mu per element
+  double* tab = nullptr;            // B then D (q x (p+1) each)
+  double* xs = nullptr;             // staging for elas_apply_host
+  double* ys = nullptr;
+  cudaStream_t stream = nullptr;
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_boundary = nullptr, ev_comm = nullptr;
+  double* halo_lo = nullptr;
+  double* halo_hi = nullptr;
+  // measurement hook
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;   // pairs (start, stop), reused
+  size_t prof_used = 0;
+  // solver state (elas_solver.cu), allocated on first use
+  int qlayout = 0;                    // qdata layout of the variant (QD_LAYOUT_*)
+  double* dinv = nullptr;             // cached 1 / diag(A) (elas_diagonal)
+  double* red = nullptr;              // reduction partials + device scalars
+  double* work = nullptr;             // 4 vectors for elas_pcg (r, z, p, t)
+};
+
+
+namespace elas {
+void free_solver_state(elas_op* op);
+// exchange the partial interface planes of y with the neighbour ranks and add them (NCCL mode,
+// synchronous on the op's stream); no-op for nranks == 1 or external mode
+int exchange_planes(elas_op* op, double* y);
+}  // namespace elas

@@ -1,0 +1,540 @@
+// Consumers of the apply in the paper's solver (PAPER.md:202-210,
+// Sec. 3.1; SPEC.md solvers): the matrix-free operator diagonal, the power-iteration estimate
+// of lambda_max(D^{-1} A), the Chebyshev polynomial smoother and preconditioned CG.  Every step
+// runs in the kernels below or in elas_apply; the host only sequences launches and reads the
+// scalar it needs for the convergence test.
+//
+// * diag_kernel (setup-time, one CTA per element): with h = grad_xi phi_I . A~ (A~ = sqrt(mu W)
+//   J^{-1}, the stored qdata), A[(c,I),(c,I)] = sum_qp (1 + r) h_c^2 + |h|^2 (r = lambda/mu).
+//   Expanding h_c^2 = sum_kl g_k g_l A~_kc A~_lc (g_k = d phi_I / d xi_k = a product of 1D B/D
+//   factors) gives, for each of the 6 pairs k <= l, a q^3 tensor
+//   M_c,kl = (1 + r) A~_kc A~_lc + (A~ A~^T)_kl contracted with the 1D product tables
+//   F_d,kl[a][i] = T_k^d[a][i] T_l^d[a][i] (T_k^d = D if k == d else B) along x, y, z in turn
+//   (sum factorisation of the diagonal, O(q^3 n) per tensor).
+// * Chebyshev (Saad, Iterative Methods, Alg. 12.1) on D^{-1} A for [alpha lam, beta lam]:
+//   two fused vector kernels per step around elas_apply.
+// * PCG: dots by a deterministic two-pass reduction into device scalars; alpha and beta are
+//   formed on the device inside the update kernels (no host round trip but the convergence
+//   read of r.z, 8 bytes per iteration).
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "elas_op.h"
+
+namespace elas {
+namespace {
+
+constexpr int RED_BLOCKS = 296;    // 2 x 148 SMs; fixed so the reduction order is fixed
+constexpr int RED_THREADS = 256;
+// device scalar slots after the RED_BLOCKS partials
+enum { S_DOT = 0, S_RZ, S_RZNEW, S_PT, S_NRM, S_LAM, S_COUNT };
+
+int fail(cudaError_t e, const char* what) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? ELAS_ENOMEM : ELAS_ECUDA;
+}
+#define CK(expr, what)                                \
+  do {                                                \
+    cudaError_t e_ = (expr);                          \
+    if (e_ != cudaSuccess) return fail(e_, what);     \
+  } while (0)
+
+#define CK_C(expr, what)                                      \
+  do {                                                        \
+    cudaError_t e_ = (expr);                                  \
+    if (e_ != cudaSuccess) return elas::fail(e_, what);       \
+  } while (0)
+
+int grid_for(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  return (int)(g < 148 * 16 ? (g > 0 ? g : 1) : 148 * 16);
+}
+
+__device__ __forceinline__ bool cons_node(int64_t node, const Slab& s) {
+  const int I = (int)(node % s.Nx), J = (int)((node / s.Nx) % s.Ny), K = (int)(node / ((int64_t)s.Nx * s.Ny));
+  const uint32_t f = s.faces;
+  return ((f & ELAS_FACE_XMIN) && I == 0) || ((f & ELAS_FACE_XMAX) && I == s.Nx - 1) ||
+         ((f & ELAS_FACE_YMIN) && J == 0) || ((f & ELAS_FACE_YMAX) && J == s.Ny - 1) ||
+         ((f & ELAS_FACE_ZMIN) && K == 0) || ((f & ELAS_FACE_ZMAX) && K == s.Nz - 1);
+}
+
+// ------------------------------------------------------------------------- diagonal
+
+// pointer to A~[f] (f = 3 k + m) at point (a1, a2, a3) of element e, for every qdata layout
+__device__ __forceinline__ const double* qd_point(const double* qd, int layout, int q, int64_t e, int a1, int a2,
+                                                  int a3, int& fstride) {
+  const int q3 = q * q * q;
+  if (layout == QD_LAYOUT_E32) {
+    fstride = 32;
+    const int pt = a1 + q * (a2 + q * a3);
+    return qd + (e >> 5) * (int64_t)(32 * 9 * q3) + (int64_t)pt * 9 * 32 + (e & 31);
+  }
+  if (layout == QD_LAYOUT_TC6) {
+    fstride = 32;
+    const int sl = a1 >> 1, r = 2 * (a1 & 1) + (a3 & 1), lane = 4 * a2 + (a3 >> 1);
+    return qd + e * (int64_t)(9 * q3) + (int64_t)((sl * 4 + r) * 9) * 32 + lane;
+  }
+  fstride = q * q;
+  return qd + e * (int64_t)qd_stride_lines(q) + (int64_t)a1 * 9 * q * q + a3 + q * a2;
+}
+
+__global__ void diag_init_kernel(Slab s, double* __restrict__ d) {
+  const int64_t n = 3 * s.nodes;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    d[t] = (s.faces && cons_node(t % s.nodes, s)) ? 1.0 : 0.0;
+}
+
+// dynamic smem: B, D (q n each), F[3] (q n each), T0[3][q^3], T1[3][q^2 n], T2[3][q n^2], acc[3][n^3]
+__global__ void __launch_bounds__(128) diag_kernel(int p, int q, int layout, Slab s, const double* __restrict__ qd,
+                                                   const double* __restrict__ rr, const double* __restrict__ tables,
+                                                   double* __restrict__ d) {
+  extern __shared__ double sm[];
+  const int n = p + 1, qn = q * n, q3 = q * q * q, n3 = n * n * n;
+  double* sB = sm;
+  double* sD = sB + qn;
+  double* F = sD + qn;              // F[dir][a][i]
+  double* T0 = F + 3 * qn;          // [c][a3][a2][a1]
+  double* T1 = T0 + 3 * q3;         // [c][a3][a2][i]
+  double* T2 = T1 + 3 * q * q * n;  // [c][a3][j][i]
+  double* acc = T2 + 3 * q * n * n; // [c][k][j][i]
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int64_t e = blockIdx.x;
+  for (int t = tid; t < 2 * qn; t += NT) sm[t] = tables[t];
+  for (int t = tid; t < 3 * n3; t += NT) acc[t] = 0.0;
+  const double r1 = 1.0 + rr[e];
+  for (int kl = 0; kl < 6; ++kl) {
+    const int k = kl < 3 ? kl : (kl == 3 ? 0 : (kl == 4 ? 0 : 1));
+    const int l = kl < 3 ? kl : (kl == 3 ? 1 : 2);
+    const double mult = (k == l) ? 1.0 : 2.0;
+    __syncthreads();   // tables loaded / previous pass done with F, T*
+    for (int t = tid; t < 3 * qn; t += NT) {
+      const int dir = t / qn, ai = t % qn;
+      const double fk = (k == dir) ? sD[ai] : sB[ai];
+      const double fl = (l == dir) ? sD[ai] : sB[ai];
+      F[t] = fk * fl;
+    }
+    for (int pt = tid; pt < q3; pt += NT) {
+      const int a1 = pt % q, a2 = (pt / q) % q, a3 = pt / (q * q);
+      int fs;
+      const double* A = qd_point(qd, layout, q, e, a1, a2, a3, fs);
+      double Ak[3], Al[3];
+      for (int m = 0; m < 3; ++m) {
+        Ak[m] = A[(3 * k + m) * fs];
+        Al[m] = A[(3 * l + m) * fs];
+      }
+      const double dot = Ak[0] * Al[0] + Ak[1] * Al[1] + Ak[2] * Al[2];
+      for (int c = 0; c < 3; ++c) T0[c * q3 + pt] = r1 * Ak[c] * Al[c] + dot;
+    }
+    __syncthreads();
+    for (int t = tid; t < 3 * q * q * n; t += NT) {   // x: a1 -> i
+      const int i = t % n, a2 = (t / n) % q, a3 = (t / (n * q)) % q, c = t / (n * q * q);
+      const double* src = T0 + c * q3 + (a3 * q + a2) * q;
+      double v = 0.0;
+      for (int a1 = 0; a1 < q; ++a1) v = fma(F[a1 * n + i], src[a1], v);
+      T1[t] = v;
+    }
+    __syncthreads();
+    for (int t = tid; t < 3 * q * n * n; t += NT) {   // y: a2 -> j
+      const int i = t % n, j = (t / n) % n, a3 = (t / (n * n)) % q, c = t / (n * n * q);
+      const double* src = T1 + ((c * q + a3) * q) * n + i;
+      double v = 0.0;
+      for (int a2 = 0; a2 < q; ++a2) v = fma(F[qn + a2 * n + j], src[a2 * n], v);
+      T2[t] = v;
+    }
+    __syncthreads();
+    for (int t = tid; t < 3 * n3; t += NT) {          // z: a3 -> k
+      const int i = t % n, j = (t / n) % n, kk = (t / (n * n)) % n, c = t / n3;
+      const double* src = T2 + (c * q) * n * n + j * n + i;
+      double v = 0.0;
+      for (int a3 = 0; a3 < q; ++a3) v = fma(F[2 * qn + a3 * n + kk], src[a3 * n * n], v);
+      acc[t] = fma(mult, v, acc[t]);
+    }
+  }
+  __syncthreads();
+  const int ex = (int)(e % s.nx), ey = (int)((e / s.nx) % s.ny), ez = (int)(e / ((int64_t)s.nx * s.ny));
+  for (int t = tid; t < 3 * n3; t += NT) {
+    const int i = t % n, j = (t / n) % n, kk = (t / (n * n)) % n, c = t / n3;
+    const int64_t node = (ex * p + i) + (int64_t)s.Nx * ((ey * p + j) + (int64_t)s.Ny * (ez * p + kk));
+    if (s.faces && cons_node(node, s)) continue;
+    atomicAdd(d + c * s.nodes + node, acc[t]);
+  }
+}
+
+// ------------------------------------------------------------------------- reductions
+
+// partial[b] = sum over this block's grid-stride share of w_i a_i b_i (w_i = 0 on interface
+// planes owned by the rank below; none for one rank)
+__global__ void __launch_bounds__(RED_THREADS) dot_partial_kernel(const double* __restrict__ a,
+                                                                  const double* __restrict__ b, int64_t n,
+                                                                  double* __restrict__ partial) {
+  __shared__ double sh[RED_THREADS];
+  double v = 0.0;
+  for (int64_t t = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x; t < n; t += (int64_t)RED_BLOCKS * RED_THREADS)
+    v = fma(a[t], b[t], v);
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = RED_THREADS / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(RED_THREADS) dot_final_kernel(const double* __restrict__ partial,
+                                                                double* __restrict__ out) {
+  __shared__ double sh[RED_THREADS];
+  double v = 0.0;
+  for (int b = threadIdx.x; b < RED_BLOCKS; b += RED_THREADS) v += partial[b];
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = RED_THREADS / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+int dot(const double* a, const double* b, int64_t n, double* red, int slot, cudaStream_t st) {
+  dot_partial_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, b, n, red);
+  dot_final_kernel<<<1, RED_THREADS, 0, st>>>(red, red + RED_BLOCKS + slot);
+  CK(cudaGetLastError(), "dot kernels");
+  return ELAS_OK;
+}
+
+// ------------------------------------------------------------------------- vector kernels
+
+__global__ void inv_kernel(const double* __restrict__ d, double* __restrict__ dinv, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    dinv[t] = 1.0 / d[t];
+}
+
+// v <- s v / sqrt(S[nrm]),  s = 1
+__global__ void normalize_kernel(double* __restrict__ v, const double* __restrict__ src, const double* __restrict__ S,
+                                 int64_t n) {
+  const double sc = 1.0 / sqrt(S[0]);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    v[t] = src[t] * sc;
+}
+
+// w = dinv * t
+__global__ void scale_kernel(double* __restrict__ w, const double* __restrict__ dinv, const double* __restrict__ t_,
+                             int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    w[t] = dinv[t] * t_[t];
+}
+
+// Chebyshev start: r = dinv (b - Ax) (Ax == nullptr: x = 0), dv = r / theta, x += dv (or x = dv)
+__global__ void cheb_start_kernel(const double* __restrict__ b, const double* __restrict__ Ax,
+                                  const double* __restrict__ dinv, double* __restrict__ r, double* __restrict__ dv,
+                                  double* __restrict__ x, double inv_theta, int zero_x, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const double rt = dinv[t] * (Ax ? b[t] - Ax[t] : b[t]);
+    const double d = rt * inv_theta;
+    r[t] = rt;
+    dv[t] = d;
+    x[t] = zero_x ? d : x[t] + d;
+  }
+}
+
+// Chebyshev step: r -= dinv Ad; dv = c1 dv + c2 r; x += dv
+__global__ void cheb_step_kernel(const double* __restrict__ Ad, const double* __restrict__ dinv,
+                                 double* __restrict__ r, double* __restrict__ dv, double* __restrict__ x, double c1,
+                                 double c2, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const double rt = r[t] - dinv[t] * Ad[t];
+    const double d = fma(c1, dv[t], c2 * rt);
+    r[t] = rt;
+    dv[t] = d;
+    x[t] += d;
+  }
+}
+
+// PCG: alpha = S[RZ] / S[PT]; x += alpha p; r -= alpha t; (jacobi) z = dinv r
+__global__ void pcg_update_kernel(double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+                                  const double* __restrict__ p, const double* __restrict__ t_,
+                                  const double* __restrict__ dinv, const double* __restrict__ S, int64_t n) {
+  const double alpha = S[S_RZ] / S[S_PT];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    x[t] = fma(alpha, p[t], x[t]);
+    const double rt = fma(-alpha, t_[t], r[t]);
+    r[t] = rt;
+    if (z) z[t] = dinv ? dinv[t] * rt : rt;
+  }
+}
+
+// PCG: beta = S[RZNEW] / S[RZ]; p = z + beta p; then S[RZ] = S[RZNEW] (one thread, after use)
+__global__ void pcg_direction_kernel(double* __restrict__ p, const double* __restrict__ z, double* __restrict__ S,
+                                     int64_t n, int first) {
+  const double beta = first ? 0.0 : S[S_RZNEW] / S[S_RZ];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    p[t] = first ? z[t] : fma(beta, p[t], z[t]);
+}
+
+__global__ void copy_scalar_kernel(double* S, int dst, int src) { S[dst] = S[src]; }
+
+// default power-iteration start vector: splitmix64 counter generator (synth.splitmix_uniform)
+__global__ void splitmix_kernel(double* __restrict__ v, int64_t n, unsigned long long seed) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long z = seed + (unsigned long long)(t + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    v[t] = 2.0 * (double)(z >> 11) * 0x1.0p-53 - 1.0;
+  }
+}
+
+int ensure_red(elas_op* op) {
+  if (!op->red) CK(cudaMalloc(&op->red, sizeof(double) * (RED_BLOCKS + S_COUNT)), "cudaMalloc (reduction scratch)");
+  return ELAS_OK;
+}
+
+int read_scalar(elas_op* op, int slot, double* out) {
+  CK(cudaMemcpyAsync(out, op->red + RED_BLOCKS + slot, sizeof(double), cudaMemcpyDeviceToHost, op->stream),
+     "cudaMemcpyAsync (scalar)");
+  CK(cudaStreamSynchronize(op->stream), "cudaStreamSynchronize");
+  return ELAS_OK;
+}
+
+int ensure_dinv(elas_op* op);
+
+}  // namespace
+
+void free_solver_state(elas_op* op) {
+  cudaFree(op->dinv);
+  cudaFree(op->red);
+  cudaFree(op->work);
+  op->dinv = op->red = op->work = nullptr;
+}
+
+}  // namespace elas
+
+struct elas_cheb {
+  elas_op* op = nullptr;
+  int order = 3;
+  double alpha = 0.1, beta = 1.1, lam_max = 0.0;
+  double* buf = nullptr;   // r, dv, t (3 vectors)
+};
+
+namespace elas {
+namespace {
+
+int diag_raw(elas_op* op, double* d) {
+  const Slab& s = op->slab;
+  const int p = op->p, q = op->q, n = p + 1;
+  const size_t smem = sizeof(double) * (size_t)(5 * q * n + 3 * (q * q * q + q * q * n + q * n * n + n * n * n));
+  static size_t attr = 0;
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "cudaFuncSetAttribute");
+    attr = smem;
+  }
+  diag_init_kernel<<<grid_for(3 * s.nodes), 256, 0, op->stream>>>(s, d);
+  const int64_t ne = (int64_t)s.nx * s.ny * s.nz;
+  if (ne > 0) diag_kernel<<<(unsigned)ne, 128, smem, op->stream>>>(p, q, op->qlayout, s, op->qd, op->rr, op->tab, d);
+  CK(cudaGetLastError(), "diagonal kernels");
+  return exchange_planes(op, d);
+}
+
+int ensure_dinv(elas_op* op) {
+  if (op->dinv) return ELAS_OK;
+  const int64_t n = 3 * op->slab.nodes;
+  double* d = nullptr;
+  CK(cudaMalloc(&d, sizeof(double) * n), "cudaMalloc (diagonal)");
+  int rc = diag_raw(op, d);
+  if (rc) { cudaFree(d); return rc; }
+  inv_kernel<<<grid_for(n), 256, 0, op->stream>>>(d, d, n);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { cudaFree(d); return fail(e, "inverse diagonal"); }
+  op->dinv = d;
+  return ELAS_OK;
+}
+
+bool solver_ok(const elas_op* op, const char* who) {
+  if (op->nranks != 1) {
+    set_error(std::string(who) + ": the solver layer supports single-GPU operators only (nranks == 1)");
+    return false;
+  }
+  return true;
+}
+
+// x <- x + p_k(D^{-1}A) D^{-1}(b - A x); x_zero: treat x as 0 on entry (preconditioner form)
+int cheb_run(elas_cheb* ch, const double* b, double* x, bool x_zero) {
+  elas_op* op = ch->op;
+  const int64_t n = 3 * op->slab.nodes;
+  double* r = ch->buf;
+  double* dv = r + n;
+  double* t = dv + n;
+  cudaStream_t st = op->stream;
+  const double lo = ch->alpha * ch->lam_max, hi = ch->beta * ch->lam_max;
+  const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo);
+  int rc;
+  if (!x_zero) {
+    if ((rc = elas_apply(op, x, t))) return rc;
+  }
+  cheb_start_kernel<<<grid_for(n), 256, 0, st>>>(b, x_zero ? nullptr : t, op->dinv, r, dv, x, 1.0 / theta,
+                                                 x_zero ? 1 : 0, n);
+  CK(cudaGetLastError(), "chebyshev start kernel");
+  if (ch->order == 1) return ELAS_OK;
+  const double sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  for (int k = 2; k <= ch->order; ++k) {
+    if ((rc = elas_apply(op, dv, t))) return rc;
+    const double rho_new = 1.0 / (2.0 * sigma - rho);
+    cheb_step_kernel<<<grid_for(n), 256, 0, st>>>(t, op->dinv, r, dv, x, rho_new * rho, 2.0 * rho_new / delta, n);
+    CK(cudaGetLastError(), "chebyshev step kernel");
+    rho = rho_new;
+  }
+  return ELAS_OK;
+}
+
+}  // namespace
+}  // namespace elas
+
+using elas::Slab;
+
+extern "C" {
+
+int elas_diagonal(elas_op* op, double* d) {
+  if (!op || !d) { elas::set_error("elas_diagonal: NULL argument"); return ELAS_EINVAL; }
+  if ((uintptr_t)d & 7u) { elas::set_error("elas_diagonal: d must be 8-byte aligned"); return ELAS_EINVAL; }
+  return elas::diag_raw(op, d);
+}
+
+elas_cheb* elas_cheb_create(elas_op* op, int order, double alpha, double beta, int power_iters, const double* v0,
+                            unsigned long long seed) {
+  if (!op) { elas::set_error("elas_cheb_create: NULL op"); return nullptr; }
+  if (!elas::solver_ok(op, "elas_cheb_create")) return nullptr;
+  if (order < 1 || power_iters < 1 || !(alpha > 0.0) || !(beta > alpha) || !std::isfinite(beta)) {
+    elas::set_error("elas_cheb_create: need order >= 1, power_iters >= 1, 0 < alpha < beta");
+    return nullptr;
+  }
+  if (elas::ensure_dinv(op) || elas::ensure_red(op)) return nullptr;
+  const int64_t n = 3 * op->slab.nodes;
+  elas_cheb* ch = new elas_cheb();
+  ch->op = op;
+  ch->order = order;
+  ch->alpha = alpha;
+  ch->beta = beta;
+  auto bail = [&](cudaError_t e, const char* what) -> elas_cheb* {
+    if (e != cudaSuccess) elas::set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    cudaFree(ch->buf);
+    delete ch;
+    return nullptr;
+  };
+  cudaError_t e = cudaMalloc(&ch->buf, sizeof(double) * 3 * n);
+  if (e != cudaSuccess) return bail(e, "cudaMalloc (chebyshev work vectors)");
+  // power iteration on D^{-1} A: v <- v/|v|; w = D^{-1} A v; lam = v.w; v <- w/|w|
+  double* v = ch->buf;
+  double* w = v + n;
+  double* t = w + n;
+  cudaStream_t st = op->stream;
+  const int g = elas::grid_for(n);
+  double* S = op->red + elas::RED_BLOCKS;
+  if (v0) e = cudaMemcpyAsync(w, v0, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+  else elas::splitmix_kernel<<<g, 256, 0, st>>>(w, n, seed);
+  if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return bail(e, "power iteration start vector");
+  if (elas::dot(w, w, n, op->red, elas::S_NRM, st)) return bail(cudaSuccess, "");
+  elas::normalize_kernel<<<g, 256, 0, st>>>(v, w, S + elas::S_NRM, n);
+  for (int it = 0; it < power_iters; ++it) {
+    if (elas_apply(op, v, t)) return bail(cudaSuccess, "");
+    elas::scale_kernel<<<g, 256, 0, st>>>(w, op->dinv, t, n);
+    if (elas::dot(v, w, n, op->red, elas::S_LAM, st) || elas::dot(w, w, n, op->red, elas::S_NRM, st))
+      return bail(cudaSuccess, "");
+    elas::normalize_kernel<<<g, 256, 0, st>>>(v, w, S + elas::S_NRM, n);
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return bail(e, "power iteration kernels");
+  double lam = 0.0;
+  if (elas::read_scalar(op, elas::S_LAM, &lam)) return bail(cudaSuccess, "");
+  if (!(lam > 0.0) || !std::isfinite(lam)) {
+    elas::set_error("elas_cheb_create: power iteration gave a non-positive estimate (zero operator?)");
+    return bail(cudaSuccess, "");
+  }
+  ch->lam_max = 1.1 * lam;
+  return ch;
+}
+
+double elas_cheb_lambda_max(const elas_cheb* ch) { return ch ? ch->lam_max : -1.0; }
+
+int elas_cheb_apply(elas_cheb* ch, const double* b, double* x) {
+  if (!ch || !b || !x) { elas::set_error("elas_cheb_apply: NULL argument"); return ELAS_EINVAL; }
+  if (b == x) { elas::set_error("elas_cheb_apply: b and x must not alias"); return ELAS_EINVAL; }
+  return elas::cheb_run(ch, b, x, false);
+}
+
+void elas_cheb_destroy(elas_cheb* ch) {
+  if (!ch) return;
+  cudaStreamSynchronize(ch->op->stream);
+  cudaFree(ch->buf);
+  delete ch;
+}
+
+int elas_pcg(elas_op* op, int precond, elas_cheb* cheb, const double* b, double* x, double rtol, int maxit,
+             elas_solve_report* rep, double* history) {
+  if (!op || !b || !x) { elas::set_error("elas_pcg: NULL argument"); return ELAS_EINVAL; }
+  if (!elas::solver_ok(op, "elas_pcg")) return ELAS_EINVAL;
+  if (precond < ELAS_PC_NONE || precond > ELAS_PC_CHEBYSHEV || (precond == ELAS_PC_CHEBYSHEV && (!cheb || cheb->op != op))) {
+    elas::set_error("elas_pcg: unknown preconditioner, or a Chebyshev preconditioner of another operator");
+    return ELAS_EINVAL;
+  }
+  if (b == x || maxit < 0 || !(rtol >= 0.0)) { elas::set_error("elas_pcg: need b != x, maxit >= 0, rtol >= 0"); return ELAS_EINVAL; }
+  int rc;
+  if ((rc = elas::ensure_red(op))) return rc;
+  if (precond == ELAS_PC_JACOBI && (rc = elas::ensure_dinv(op))) return rc;
+  const int64_t n = 3 * op->slab.nodes;
+  if (!op->work) CK_C(cudaMalloc(&op->work, sizeof(double) * 4 * n), "cudaMalloc (pcg work vectors)");
+  double* r = op->work;
+  double* z = r + n;
+  double* p = z + n;
+  double* t = p + n;
+  cudaStream_t st = op->stream;
+  const int g = elas::grid_for(n);
+  double* S = op->red + elas::RED_BLOCKS;
+  // x = 0, r = b, z = M r
+  CK_C(cudaMemsetAsync(x, 0, sizeof(double) * n, st), "cudaMemsetAsync");
+  CK_C(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
+  auto precondition = [&]() -> int {
+    if (precond == ELAS_PC_CHEBYSHEV) return elas::cheb_run(cheb, r, z, true);
+    if (precond == ELAS_PC_JACOBI) elas::scale_kernel<<<g, 256, 0, st>>>(z, op->dinv, r, n);
+    else CK_C(cudaMemcpyAsync(z, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
+    CK_C(cudaGetLastError(), "preconditioner kernel");
+    return ELAS_OK;
+  };
+  if ((rc = precondition())) return rc;
+  if ((rc = elas::dot(r, z, n, op->red, elas::S_RZ, st))) return rc;
+  double rz0 = 0.0;
+  if ((rc = elas::read_scalar(op, elas::S_RZ, &rz0))) return rc;
+  int it = 0;
+  double rel = rz0 > 0.0 ? 1.0 : 0.0;
+  if (history && maxit >= 0) history[0] = rel;
+  if (rz0 < 0.0 || !std::isfinite(rz0)) { elas::set_error("elas_pcg: preconditioner not positive definite"); return ELAS_EINVAL; }
+  if (rz0 > 0.0) {
+    elas::pcg_direction_kernel<<<g, 256, 0, st>>>(p, z, S, n, 1);
+    while (it < maxit) {
+      if ((rc = elas_apply(op, p, t))) return rc;
+      if ((rc = elas::dot(p, t, n, op->red, elas::S_PT, st))) return rc;
+      const bool fused_z = precond != ELAS_PC_CHEBYSHEV;
+      elas::pcg_update_kernel<<<g, 256, 0, st>>>(x, r, fused_z ? z : nullptr, p, t,
+                                                 precond == ELAS_PC_JACOBI ? op->dinv : nullptr, S, n);
+      CK_C(cudaGetLastError(), "pcg update kernel");
+      if (!fused_z && (rc = elas::cheb_run(cheb, r, z, true))) return rc;
+      if ((rc = elas::dot(r, z, n, op->red, elas::S_RZNEW, st))) return rc;
+      double rz = 0.0;
+      if ((rc = elas::read_scalar(op, elas::S_RZNEW, &rz))) return rc;
+      ++it;
+      rel = std::sqrt(rz > 0.0 ? rz / rz0 : 0.0);
+      if (history) history[it] = rel;
+      if (rel <= rtol) break;
+      elas::pcg_direction_kernel<<<g, 256, 0, st>>>(p, z, S, n, 0);
+      elas::copy_scalar_kernel<<<1, 1, 0, st>>>(S, elas::S_RZ, elas::S_RZNEW);
+      CK_C(cudaGetLastError(), "pcg direction kernels");
+    }
+  }
+  if (rep) {
+    rep->iterations = it;
+    rep->rel_residual = rel;
+    rep->converged = rel <= rtol ? 1 : 0;
+  }
+  return ELAS_OK;
+}
+
+}  // extern "C"

@@ -10,6 +10,7 @@ convenience wrapper that owns the handle.  Device arrays are passed as torch CUD
 """
 
 import ctypes
+import weakref
 import os
 
 import numpy as np
@@ -24,13 +25,20 @@ FACE_XMIN, FACE_XMAX, FACE_YMIN, FACE_YMAX, FACE_ZMIN, FACE_ZMAX = 1, 2, 4, 8, 1
 EXPORTED = ["elas_create", "elas_apply", "elas_apply_host", "elas_interface_add", "elas_destroy",
             "elas_local_dofs", "elas_local_zrange", "elas_set_stream", "elas_launches_per_apply",
             "elas_last_error", "elas_slab_range", "elas_tables", "elas_nccl_unique_id", "elas_version",
-            "elas_profile", "elas_profile_read", "elas_create_ex", "elas_variant"]
+            "elas_profile", "elas_profile_read", "elas_create_ex", "elas_variant",
+            "elas_diagonal", "elas_cheb_create", "elas_cheb_lambda_max", "elas_cheb_apply",
+            "elas_cheb_destroy", "elas_pcg"]
+PC_NONE, PC_JACOBI, PC_CHEBYSHEV = 0, 1, 2
 
 
 class ElasError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"elas error {code}: {msg}")
         self.code = code
+
+
+class elas_solve_report(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int), ("converged", ctypes.c_int), ("rel_residual", ctypes.c_double)]
 
 
 class elas_mesh(ctypes.Structure):
@@ -90,6 +98,20 @@ def load(path=None):
     lib.elas_profile.argtypes = [P, ctypes.c_int]
     lib.elas_profile_read.restype = ctypes.c_int
     lib.elas_profile_read.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]
+    lib.elas_diagonal.restype = ctypes.c_int
+    lib.elas_diagonal.argtypes = [P, P]
+    lib.elas_cheb_create.restype = P
+    lib.elas_cheb_create.argtypes = [P, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int, P,
+                                     ctypes.c_ulonglong]
+    lib.elas_cheb_lambda_max.restype = ctypes.c_double
+    lib.elas_cheb_lambda_max.argtypes = [P]
+    lib.elas_cheb_apply.restype = ctypes.c_int
+    lib.elas_cheb_apply.argtypes = [P, P, P]
+    lib.elas_cheb_destroy.restype = None
+    lib.elas_cheb_destroy.argtypes = [P]
+    lib.elas_pcg.restype = ctypes.c_int
+    lib.elas_pcg.argtypes = [P, ctypes.c_int, P, P, P, ctypes.c_double, ctypes.c_int,
+                             ctypes.POINTER(elas_solve_report), D]
     _lib = lib
     return lib
 
@@ -241,6 +263,39 @@ def elas_launches_per_apply(h):
     return load().elas_launches_per_apply(h)
 
 
+def elas_diagonal(h, d):
+    _check(load().elas_diagonal(h, _ptr(d)), "elas_diagonal")
+
+
+def elas_cheb_create(h, order=3, alpha=0.1, beta=1.1, power_iters=10, v0=None, seed=0):
+    c = load().elas_cheb_create(h, order, alpha, beta, power_iters, _ptr(v0), seed)
+    if not c:
+        raise ElasError(ELAS_EINVAL, f"elas_cheb_create: {elas_last_error()}")
+    return c
+
+
+def elas_cheb_lambda_max(c):
+    return load().elas_cheb_lambda_max(c)
+
+
+def elas_cheb_apply(c, b, x):
+    _check(load().elas_cheb_apply(c, _ptr(b), _ptr(x)), "elas_cheb_apply")
+
+
+def elas_cheb_destroy(c):
+    load().elas_cheb_destroy(c)
+
+
+def elas_pcg(h, precond, cheb, b, x, rtol, maxit, history=False):
+    """Returns (iterations, converged, rel_residual, history array or None)."""
+    import numpy as np
+    rep = elas_solve_report()
+    hist = np.zeros(maxit + 1) if history else None
+    _check(load().elas_pcg(h, precond, cheb, _ptr(b), _ptr(x), rtol, maxit, ctypes.byref(rep),
+                           _dptr(hist) if history else None), "elas_pcg")
+    return rep.iterations, bool(rep.converged), rep.rel_residual, (hist[:rep.iterations + 1] if history else None)
+
+
 # ------------------------------------------------------------------ convenience wrapper
 
 class Operator:
@@ -258,6 +313,7 @@ class Operator:
         elas_set_stream(self.h, stream)
         self.local_dofs = elas_local_dofs(self.h)
         self.zrange = elas_local_zrange(self.h)
+        self._chebs = []
 
     @classmethod
     def from_problem(cls, P, rank=0, nranks=1, nccl_id=None, stream=None, variant=VARIANT_AUTO):
@@ -278,13 +334,51 @@ class Operator:
     def set_stream(self, stream):
         elas_set_stream(self.h, stream)
 
+    def diagonal(self, d):
+        elas_diagonal(self.h, d)
+
+    def chebyshev(self, order=3, alpha=0.1, beta=1.1, power_iters=10, v0=None, seed=0):
+        c = Chebyshev(self, order, alpha, beta, power_iters, v0, seed)
+        self._chebs.append(weakref.ref(c))
+        return c
+
+    def pcg(self, b, x, precond=PC_JACOBI, cheb=None, rtol=1e-8, maxit=1000, history=False):
+        return elas_pcg(self.h, precond, cheb.h if cheb is not None else None, b, x, rtol, maxit, history)
+
     @property
     def launches_per_apply(self):
         return elas_launches_per_apply(self.h)
 
     def close(self):
         if self.h:
+            for ref in getattr(self, "_chebs", []):   # smoothers hold the op: destroy them first
+                c = ref()
+                if c is not None:
+                    c.close()
             elas_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Chebyshev:
+    """Owns one elas_cheb handle (smoother / preconditioner of an Operator)."""
+
+    def __init__(self, op, order=3, alpha=0.1, beta=1.1, power_iters=10, v0=None, seed=0):
+        self.op = op
+        self.h = elas_cheb_create(op.h, order, alpha, beta, power_iters, v0, seed)
+        self.lambda_max = elas_cheb_lambda_max(self.h)
+
+    def apply(self, b, x):
+        elas_cheb_apply(self.h, b, x)
+
+    def close(self):
+        if self.h:
+            elas_cheb_destroy(self.h)
             self.h = None
 
     def __del__(self):
