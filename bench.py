@@ -237,6 +237,55 @@ def sweep_config4(reps=10, warmup=3):
     return out
 
 
+# ------------------------------------------------------------------------------ solver row
+
+def solver_bench(cfg=3, passes=10, rtol=1e-8, maxit=4000):
+    """SURVEY 8(f) NEXT rank 1-2 on the GPU: diagonal + power-iteration setup, Chebyshev
+    smoothing passes (order 3: 3 applies + 3 fused vector kernels each) and PCG to rtol with
+    Chebyshev and Jacobi preconditioning.  Solver throughput as PAPER.md:386 defines it:
+    "total degrees of freedom processed per second" = N_dof x iterations / solve time."""
+    import torch
+    import synth
+    from paper_2601_08374_b200.elas import Operator, PC_JACOBI, PC_CHEBYSHEV
+    P = synth.make_config(cfg, draw_x=False)
+    op = Operator.from_problem(P)
+    n = P.num_dofs
+    b = torch.from_numpy(synth.splitmix_uniform(n, 11)).cuda()
+    x = torch.zeros_like(b)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    ch = op.chebyshev(order=3, alpha=0.1, beta=1.1, power_iters=10, seed=1)
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t
+    ch.apply(b, x)
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(passes):
+        ch.apply(b, x)
+    e.record()
+    torch.cuda.synchronize()
+    pass_ms = a.elapsed_time(e) / passes
+    out = {"workload": workload_desc(P), "chebyshev": {"order": 3, "interval": "[0.1, 1.1] x lambda_max",
+           "lambda_max": round(ch.lambda_max, 6), "setup_s_diag_plus_10_power_its": round(setup, 4),
+           "ms_per_pass": round(pass_ms, 4), "applies_per_pass": 3,
+           "gdofs_per_apply_equiv": round(3 * n / (pass_ms / 1e3) / 1e9, 3)}}
+    for name, pc in (("pcg_chebyshev", PC_CHEBYSHEV), ("pcg_jacobi", PC_JACOBI)):
+        op.pcg(b, x, precond=pc, cheb=ch, rtol=rtol, maxit=3)   # warm
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        it, conv, rel, _ = op.pcg(b, x, precond=pc, cheb=ch, rtol=rtol, maxit=maxit)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t
+        out[name] = {"rtol": rtol, "iterations": it, "converged": conv, "rel_residual": rel,
+                     "solve_s": round(dt, 4), "ms_per_iteration": round(dt / max(it, 1) * 1e3, 4),
+                     "solver_mdofs": round(n * it / dt / 1e6, 1)}
+    ch.close()
+    op.close()
+    torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------------------------ arms
 
 def run_ours(args):
@@ -350,6 +399,8 @@ def run_ours(args):
     torch.cuda.empty_cache()
     if ws == 1 and rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(P)
+    if ws == 1 and not args.no_solver:
+        line["solver"] = solver_bench()
     if ws == 1 and not args.no_sweep:
         line["sweep"] = {"workload": "config 4: m^3 unit cube, m = round(255.44/p), q=p+2, affine, lam=1, mu=0.5, seed 3",
                          "per_p": sweep_config4()}
@@ -399,6 +450,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-solver", action="store_true")
     ap.add_argument("--ref-elems", type=int, default=0)
     args = ap.parse_args()
     if args.warmup < 3:
