@@ -184,11 +184,31 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
 #pragma unroll
     for (int a1 = 0; a1 < R - 1; ++a1) ring_issue(a1);
   }
+  // Stage-Z gather issued before the table copy and the first barrier so that both global
+  // latencies overlap (EB n^2 <= NT: at most one z-column per thread).  Element coordinates in
+  // 32-bit arithmetic (element ids < 2^31).
+  static_assert(EB * N * N <= NT, "stage Z assumes at most one z-column per thread");
+  const int64_t plane = (int64_t)s.Nx * s.Ny;
+  const bool bc = s.faces != 0;
+  const bool zcol = tid < ne * N * N;
+  const int zi = tid % N, zj = (tid / N) % N, zel = tid / (N * N);
+  double u[3][N];
+  if (zcol) {
+    const uint32_t e32 = (uint32_t)(e0 + zel), nx = (uint32_t)s.nx, ny = (uint32_t)s.ny;
+    const uint32_t exy = e32 / nx, ex = e32 - exy * nx, ez = exy / ny, ey = exy - ez * ny;
+    const int I = (int)ex * P + zi, J = (int)ey * P + zj;
+    const int64_t base = I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const bool cons = bc && is_constrained(I, J, (int)ez * P + k, s);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) u[c][k] = cons ? 0.0 : __ldg(x + c * s.nodes + base + k * plane);
+    }
+  }
   {
     const double* ft = tables + 2 * Q * N;   // fold(B) | fold(D) follow the plain tables
     for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = ft[t];
   }
-  const int64_t plane = (int64_t)s.Nx * s.Ny;
 #if ELAS_L2_PREFETCH
   if (tid == 0 && pref_ctas > 0) {
     const int64_t pe0 = e0 + (int64_t)pref_ctas * EB;
@@ -201,23 +221,11 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
     }
   }
 #endif
-  const bool bc = s.faces != 0;
   __syncthreads();
 
-  // ---------------- Stage Z: gather + folded contraction in z ---------------------------
-  for (int w = tid; w < ne * N * N; w += NT) {
-    const int i = w % N, j = (w / N) % N, el = w / (N * N);
-    const int64_t e = e0 + el;
-    const int ex = (int)(e % s.nx), ey = (int)((e / s.nx) % s.ny), ez = (int)(e / ((int64_t)s.nx * s.ny));
-    const int I = ex * P + i, J = ey * P + j;
-    const int64_t base = I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
-    double u[3][N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      const bool cons = bc && is_constrained(I, J, ez * P + k, s);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) u[c][k] = cons ? 0.0 : __ldg(x + c * s.nodes + base + k * plane);
-    }
+  // ---------------- Stage Z: folded contraction in z of the gathered column -------------
+  if (zcol) {
+    const int i = zi, j = zj, el = zel;
     double up[3][NE], um[3][NHX];
     fold_in<N, NE, NHX>(u, up, um);
     double* dst = sZ + el * C::ZE + j * N + i;
@@ -537,8 +545,9 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
   // ---------------- Stage Zt: folded transposed contraction in z + scatter-add ----------
   for (int w = tid; w < ne * N * N; w += NT) {
     const int i = w % N, j = (w / N) % N, el = w / (N * N);
-    const int64_t e = e0 + el;
-    const int ex = (int)(e % s.nx), ey = (int)((e / s.nx) % s.ny), ez = (int)(e / ((int64_t)s.nx * s.ny));
+    const uint32_t e32 = (uint32_t)(e0 + el), nxu = (uint32_t)s.nx, nyu = (uint32_t)s.ny;
+    const uint32_t exy = e32 / nxu;
+    const int ex = (int)(e32 - exy * nxu), ez = (int)(exy / nyu), ey = (int)(exy - (uint32_t)ez * nyu);
     const double* src = sZ + el * C::ZE + j * N + i;
     double X[3][NE], Y[3][NE];
 #pragma unroll
