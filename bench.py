@@ -198,14 +198,21 @@ def barrier(ws):
 
 # ------------------------------------------------------------------------------ sweep
 
-def sweep_config4(reps=10, warmup=3):
+PEAK_FP32_DERIVED = 148 * 128 * 2 * 1.965e9    # FFMA/clk/SM x 2 flop x SMs x max clock
+
+
+def sweep_config4(reps=10, warmup=3, variant=0, ps=range(1, 9)):
+    """variant 0: AUTO (FP64).  variant 5: the mixed-precision folded kernel (FP32 qdata and
+    arithmetic, FP64 vectors): roofline against the FP32 pipe and 36 B of qdata per point."""
     import torch
     import synth
     from paper_2601_08374_b200.elas import Operator, elas_profile, elas_profile_read
+    f32 = variant == 5
+    peak = PEAK_FP32_DERIVED if f32 else PEAK_FP64_DERIVED
     out = {}
-    for p in range(1, 9):
+    for p in ps:
         P = synth.make_config(4, p)
-        op = Operator.from_problem(P)
+        op = Operator.from_problem(P, variant=variant)
         x = torch.from_numpy(P.x).cuda()
         y = torch.empty_like(x)
         for _ in range(warmup):
@@ -224,13 +231,15 @@ def sweep_config4(reps=10, warmup=3):
         tk = kms / nl / 1e3
         F = alg_flops(p, P.q, P.num_elements)
         B = alg_bytes(P.num_dofs, P.num_elements, P.q, False)
-        roof_t = max(F / PEAK_FP64_DERIVED, B / 8e12)
+        if f32:
+            B = 16 * P.num_dofs + 36 * P.q ** 3 * P.num_elements
+        roof_t = max(F / peak, B / 8e12)
         out[str(p)] = {"q": P.q, "dofs": P.num_dofs, "elements": P.num_elements,
                        "gdofs": round(P.num_dofs / t / 1e9, 3), "ms_per_apply": round(t * 1e3, 4),
                        "kernel_ms": round(tk * 1e3, 4),
-                       "fp64_tflops_alg": round(F / tk / 1e12, 2),
+                       ("fp32" if f32 else "fp64") + "_tflops_alg": round(F / tk / 1e12, 2),
                        "roofline_frac": round(roof_t / t, 4),
-                       "bound": "fp64" if F / PEAK_FP64_DERIVED > B / 8e12 else "hbm"}
+                       "bound": ("fp32" if f32 else "fp64") if F / peak > B / 8e12 else "hbm"}
         op.close()
         del x, y
         torch.cuda.empty_cache()
@@ -404,6 +413,11 @@ def run_ours(args):
     if ws == 1 and not args.no_sweep:
         line["sweep"] = {"workload": "config 4: m^3 unit cube, m = round(255.44/p), q=p+2, affine, lam=1, mu=0.5, seed 3",
                          "per_p": sweep_config4()}
+        line["sweep_mixed_precision"] = {
+            "workload": "config 4 as above, ELAS_VARIANT_FOLDED_F32 (FP32 qdata/tables/arithmetic, FP64 x, y, scatter; "
+                        "rel. L2 vs oracle <= 1e-5, not the FP64 contract); roofline: FP32 pipe 74.4 TF derived, "
+                        "16 B/DoF + 36 B/point",
+            "per_p": sweep_config4(variant=5, ps=range(2, 9))}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

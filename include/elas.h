@@ -90,6 +90,11 @@ elas_op* elas_create(const elas_mesh* mesh, int p, int q, const double* lambda, 
  *   ELAS_VARIANT_THREAD one thread per element, sum factorisation in registers (p = 1 only);
  *   ELAS_VARIANT_FOLDED the SIMT kernel with even-odd folded 1D contractions (every p, q;
  *                       half the sum-factorisation FMAs; same qdata layout as SIMT);
+ *   ELAS_VARIANT_FOLDED_F32  MIXED PRECISION (PAPER.md:600 future work): the folded kernel
+ *                       with FP32 quadrature data (9 floats per point), FP32 tables and FP32
+ *                       arithmetic; x, y stay FP64 (converted on gather, FP64 atomics on
+ *                       scatter).  Accuracy ~1e-6 relative, not the FP64 1e-12 (DESIGN.md
+ *                       section 11); never chosen by AUTO.
  *   ELAS_VARIANT_AUTO   the faster measured variant for (p, q).
  * The choice fixes the quadrature-data layout, so it is made at creation. */
 #define ELAS_VARIANT_AUTO 0
@@ -97,13 +102,14 @@ elas_op* elas_create(const elas_mesh* mesh, int p, int q, const double* lambda, 
 #define ELAS_VARIANT_TENSOR 2
 #define ELAS_VARIANT_THREAD 3
 #define ELAS_VARIANT_FOLDED 4
+#define ELAS_VARIANT_FOLDED_F32 5
 
 /* elas_create with an explicit kernel variant; NULL + ELAS_EINVAL message if the variant
  * does not exist for (p, q). */
 elas_op* elas_create_ex(const elas_mesh* mesh, int p, int q, const double* lambda, const double* mu,
                         int variant);
 
-/* The resolved variant of an op (ELAS_VARIANT_SIMT, _TENSOR, _THREAD or _FOLDED), -1 if NULL. */
+/* The resolved variant of an op (ELAS_VARIANT_SIMT, _TENSOR, _THREAD, _FOLDED or _FOLDED_F32), -1 if NULL. */
 int elas_variant(const elas_op* op);
 
 /* y = A x (overwrite), or y = Z A Z x + (I - Z) x with Dirichlet faces.
@@ -181,7 +187,8 @@ void elas_cheb_destroy(elas_cheb* ch);   /* NULL-safe; synchronises the op's str
 
 /* Preconditioned conjugate gradients from x = 0 (single-GPU operators).  precond:
  * ELAS_PC_NONE, ELAS_PC_JACOBI (D^{-1}, cached in the op) or ELAS_PC_CHEBYSHEV (z =
- * p_k(D^{-1}A) D^{-1} r, `cheb` of the same op).  Stops when sqrt(r.z / r0.z0) <= rtol or after
+ * p_k(D^{-1}A) D^{-1} r with `cheb`'s operator, which may be another op of the same mesh and
+ * stream -- e.g. an ELAS_VARIANT_FOLDED_F32 op: FP64 CG with a mixed-precision smoother).  Stops when sqrt(r.z / r0.z0) <= rtol or after
  * maxit iterations (not an error: report.converged = 0).  history (HOST, maxit + 1 doubles or
  * NULL) receives sqrt(r_i.z_i / r0.z0).  Synchronises once per iteration (8-byte read of r.z).
  * Dots are deterministic (fixed two-pass reduction order).  ELAS_OK / ELAS_EINVAL (bad

@@ -44,10 +44,10 @@ thread_local std::string g_err;
 DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
 #undef DECL
 #define DECL(P)                                                                                  \
-  cudaError_t apply_eo_info_p##P(int q, ApplyLaunch* info);                                      \
-  cudaError_t apply_eo_launch_p##P(int q, const Slab& s, const double* x, double* y, const double* qd, \
-                                   const double* rr, const double* tables, int64_t e_begin,     \
-                                   int64_t e_end, cudaStream_t st);
+  cudaError_t apply_eo_info_p##P(int q, int fp32, ApplyLaunch* info);                            \
+  cudaError_t apply_eo_launch_p##P(int q, int fp32, const Slab& s, const double* x, double* y,   \
+                                   const void* qd, const double* rr, const void* tables,        \
+                                   int64_t e_begin, int64_t e_end, cudaStream_t st);
 DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
 #undef DECL
 
@@ -78,20 +78,20 @@ cudaError_t apply_launch(int p, int q, const Slab& s, const double* x, double* y
   }
 }
 
-cudaError_t apply_eo_info(int p, int q, ApplyLaunch* info) {
+cudaError_t apply_eo_info(int p, int q, int fp32, ApplyLaunch* info) {
   switch (p) {
-#define CASE(P) case P: return apply_eo_info_p##P(q, info);
+#define CASE(P) case P: return apply_eo_info_p##P(q, fp32, info);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t apply_eo_launch(int p, int q, const Slab& s, const double* x, double* y, const double* qd,
-                            const double* rr, const double* tables, int64_t e_begin, int64_t e_end,
+cudaError_t apply_eo_launch(int p, int q, int fp32, const Slab& s, const double* x, double* y, const void* qd,
+                            const double* rr, const void* tables, int64_t e_begin, int64_t e_end,
                             cudaStream_t st) {
   switch (p) {
-#define CASE(P) case P: return apply_eo_launch_p##P(q, s, x, y, qd, rr, tables, e_begin, e_end, st);
+#define CASE(P) case P: return apply_eo_launch_p##P(q, fp32, s, x, y, qd, rr, tables, e_begin, e_end, st);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
     default: return cudaErrorInvalidValue;
@@ -133,6 +133,7 @@ void free_op(elas_op* op) {
   cudaFree(op->qd);
   cudaFree(op->rr);
   cudaFree(op->tab);
+  cudaFree(op->tabf);
   cudaFree(op->xs);
   cudaFree(op->ys);
   cudaFree(op->halo_lo);
@@ -215,11 +216,12 @@ int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* m
     cudaFree(dbad);
   };
   cudaError_t e;
-  const int qlayout = op->variant == ELAS_VARIANT_TENSOR   ? elas::QD_LAYOUT_TC6
-                      : op->variant == ELAS_VARIANT_THREAD ? elas::QD_LAYOUT_E32
-                                                           : elas::QD_LAYOUT_LINES;
+  const int qlayout = op->variant == ELAS_VARIANT_TENSOR        ? elas::QD_LAYOUT_TC6
+                      : op->variant == ELAS_VARIANT_THREAD      ? elas::QD_LAYOUT_E32
+                      : op->variant == ELAS_VARIANT_FOLDED_F32 ? elas::QD_LAYOUT_LINES_F32
+                                                                : elas::QD_LAYOUT_LINES;
   op->qlayout = qlayout;
-  const size_t qbytes = sizeof(double) * (size_t)elas::qd_stride(q, qlayout) * (size_t)elas::qd_elems(ne, qlayout);
+  const size_t qbytes = elas::qd_word_bytes(qlayout) * (size_t)elas::qd_stride(q, qlayout) * (size_t)elas::qd_elems(ne, qlayout);
   if ((e = cudaMalloc(&op->qd, qbytes)) != cudaSuccess ||
       (e = cudaMalloc(&op->rr, sizeof(double) * ne)) != cudaSuccess ||
       (e = cudaMalloc(&op->tab, sizeof(double) * tabh.size())) != cudaSuccess ||
@@ -232,7 +234,10 @@ int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* m
   }
   int rc = ELAS_OK;
   do {
-    if ((e = cudaMemcpy(op->tab, tabh.data(), sizeof(double) * tabh.size(), cudaMemcpyHostToDevice)) ||
+    std::vector<float> tabf(tabh.begin(), tabh.end());
+    if ((e = cudaMalloc(&op->tabf, sizeof(float) * tabf.size())) ||
+        (e = cudaMemcpy(op->tabf, tabf.data(), sizeof(float) * tabf.size(), cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(op->tab, tabh.data(), sizeof(double) * tabh.size(), cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(dV, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(dlam, lam.data(), sizeof(double) * ne, cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(dmu, muv.data(), sizeof(double) * ne, cudaMemcpyHostToDevice)) ||
@@ -278,7 +283,9 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
                   : op->variant == ELAS_VARIANT_THREAD
                       ? elas::apply_p1t_launch(op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
                   : op->variant == ELAS_VARIANT_FOLDED
-                      ? elas::apply_eo_launch(op->p, op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
+                      ? elas::apply_eo_launch(op->p, op->q, 0, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
+                  : op->variant == ELAS_VARIANT_FOLDED_F32
+                      ? elas::apply_eo_launch(op->p, op->q, 1, op->slab, x, y, op->qd, op->rr, op->tabf, e0, e1, st)
                       : elas::apply_launch(op->p, op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st);
   if (e != cudaSuccess) return cuda_fail(e, "apply kernel launch");
   if (op->prof) CUDA_OR(cudaEventRecord(ev1, st), "cudaEventRecord");
@@ -356,7 +363,7 @@ elas_op* elas_create(const elas_mesh* m, int p, int q, const double* lambda, con
 
 elas_op* elas_create_ex(const elas_mesh* m, int p, int q, const double* lambda, const double* mu, int variant) {
   elas::g_err.clear();
-  if (variant < ELAS_VARIANT_AUTO || variant > ELAS_VARIANT_FOLDED) {
+  if (variant < ELAS_VARIANT_AUTO || variant > ELAS_VARIANT_FOLDED_F32) {
     set_error("elas_create_ex: unknown variant");
     return nullptr;
   }

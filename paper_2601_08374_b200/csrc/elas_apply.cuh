@@ -33,17 +33,18 @@ namespace elas {
 // compile-time layout search: minimise 128-byte wavefronts of 64-bit shared accesses
 // (half-warp of 16 lanes, bank = double word mod 16, equal addresses broadcast)
 // ---------------------------------------------------------------------------------------
-constexpr int halfwarp_cost(const int* addr, int n) {
+// G = lanes per 128-byte wavefront = number of word-banks: 16 for 8-byte words, 32 for 4-byte
+constexpr int halfwarp_cost(const int* addr, int n, int G = 16) {
   int total = 0;
-  for (int h = 0; h < n; h += 16) {
-    int cnt[16] = {0};
+  for (int h = 0; h < n; h += G) {
+    int cnt[32] = {0};
     int worst = 0;
-    for (int l = h; l < h + 16 && l < n; ++l) {
+    for (int l = h; l < h + G && l < n; ++l) {
       bool dup = false;
       for (int m = h; m < l; ++m)
         if (addr[m] == addr[l]) dup = true;
       if (dup) continue;
-      int b = ((addr[l] % 16) + 16) % 16;
+      int b = ((addr[l] % G) + G) % G;
       cnt[b] += 1;
       if (cnt[b] > worst) worst = cnt[b];
     }
@@ -53,28 +54,28 @@ constexpr int halfwarp_cost(const int* addr, int n) {
 }
 
 // a3-stride of the Z buffer: stage Y/Yt lanes are (i fast, a3 slow)
-constexpr int pick_SA(int N, int Q) {
+constexpr int pick_SA(int N, int Q, int G = 16) {
   int best = N * N, best_cost = 1 << 30;
-  for (int SA = N * N; SA < N * N + 16; ++SA) {
+  for (int SA = N * N; SA < N * N + G; ++SA) {
     int addr[512] = {0};
     int n = 0;
     for (int a3 = 0; a3 < Q; ++a3)
       for (int i = 0; i < N; ++i) addr[n++] = a3 * SA + i;
-    int c = halfwarp_cost(addr, n);
+    int c = halfwarp_cost(addr, n, G);
     if (c < best_cost) { best_cost = c; best = SA; }
   }
   return best;
 }
 
 // a2-stride of the Y buffer: stage X lanes are lines L = a3 + Q a2 (a3 fast)
-constexpr int pick_S2(int N, int Q) {
+constexpr int pick_S2(int N, int Q, int G = 16) {
   int best = Q * N, best_cost = 1 << 30;
-  for (int S2 = Q * N; S2 < Q * N + 16; ++S2) {
+  for (int S2 = Q * N; S2 < Q * N + G; ++S2) {
     int addr[512] = {0};
     int n = 0;
     for (int a2 = 0; a2 < Q; ++a2)
       for (int a3 = 0; a3 < Q; ++a3) addr[n++] = a2 * S2 + a3 * N;
-    int c = halfwarp_cost(addr, n);
+    int c = halfwarp_cost(addr, n, G);
     if (c < best_cost) { best_cost = c; best = S2; }
   }
   return best;
@@ -82,37 +83,37 @@ constexpr int pick_S2(int N, int Q) {
 
 // element strides of the Z and Y buffers: at low order one warp spans several elements, so
 // pad the element strides to minimise conflicts over whole warps of every stage's pattern
-constexpr int elem_pattern_cost(int N, int Q, int SA, int S2, int ZE, int YE, int NT) {
+constexpr int elem_pattern_cost(int N, int Q, int SA, int S2, int ZE, int YE, int NT, int G = 16) {
   int total = 0;
   int addr[512] = {0};
   const int lanes = NT < 512 ? NT : 512;
   // stage Z / Zt: Z buffer, lanes (i, j, el)
   for (int w = 0; w < lanes; ++w) addr[w] = (w / (N * N)) * ZE + ((w / N) % N) * N + w % N;
-  total += halfwarp_cost(addr, lanes);
+  total += halfwarp_cost(addr, lanes, G);
   // stage Y / Yt: Z buffer and Y buffer, lanes (i, a3, el)
   for (int w = 0; w < lanes; ++w) addr[w] = (w / (N * Q)) * ZE + ((w / N) % Q) * SA + w % N;
-  total += halfwarp_cost(addr, lanes);
+  total += halfwarp_cost(addr, lanes, G);
   for (int w = 0; w < lanes; ++w) addr[w] = (w / (N * Q)) * YE + ((w / N) % Q) * N + w % N;
-  total += halfwarp_cost(addr, lanes);
+  total += halfwarp_cost(addr, lanes, G);
   // stage X: Y buffer, lanes (a3, a2, el)
   for (int w = 0; w < lanes; ++w) addr[w] = (w / (Q * Q)) * YE + ((w / Q) % Q) * S2 + (w % Q) * N;
-  total += halfwarp_cost(addr, lanes);
+  total += halfwarp_cost(addr, lanes, G);
   return total;
 }
 
-constexpr int pick_ZE(int N, int Q, int SA, int S2, int ZE0, int YE0, int NT) {
+constexpr int pick_ZE(int N, int Q, int SA, int S2, int ZE0, int YE0, int NT, int G = 16) {
   int best = ZE0, bc = 1 << 30;
-  for (int p = 0; p < 16; ++p) {
-    const int c = elem_pattern_cost(N, Q, SA, S2, ZE0 + p, YE0, NT);
+  for (int p = 0; p < G; ++p) {
+    const int c = elem_pattern_cost(N, Q, SA, S2, ZE0 + p, YE0, NT, G);
     if (c < bc) { bc = c; best = ZE0 + p; }
   }
   return best;
 }
 
-constexpr int pick_YE(int N, int Q, int SA, int S2, int ZE, int YE0, int NT) {
+constexpr int pick_YE(int N, int Q, int SA, int S2, int ZE, int YE0, int NT, int G = 16) {
   int best = YE0, bc = 1 << 30;
-  for (int p = 0; p < 16; ++p) {
-    const int c = elem_pattern_cost(N, Q, SA, S2, ZE, YE0 + p, NT);
+  for (int p = 0; p < G; ++p) {
+    const int c = elem_pattern_cost(N, Q, SA, S2, ZE, YE0 + p, NT, G);
     if (c < bc) { bc = c; best = YE0 + p; }
   }
   return best;
@@ -137,32 +138,38 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 #define ELAS_NT 128
 #endif
 
-template <int P, int Q, int TABSZ = 2 * Q * (P + 1), int NTHR = ELAS_NT>
+// WB: bytes per stored word (8: FP64 kernels; 4: the FP32 folded kernel).  All counts below
+// are in words of that size.
+constexpr int qd_stride_words(int q, int WB) { return WB == 8 ? (9 * q * q * q + 1) & ~1 : (9 * q * q * q + 3) & ~3; }
+
+template <int P, int Q, int TABSZ = 2 * Q * (P + 1), int NTHR = ELAS_NT, int WB = 8>
 struct Cfg {
   static constexpr int N = P + 1;
   static constexpr int NT = NTHR;
-  static constexpr int SA = pick_SA(N, Q);
+  static constexpr int G = 128 / WB;       // word-banks per wavefront
+  static constexpr int AL = 16 / WB;       // words per 16 bytes
+  static constexpr int SA = pick_SA(N, Q, G);
   static constexpr int ZV = Q * SA;        // variant stride (Zb | Zd)
   static constexpr int ZC = 2 * ZV;        // component stride
-  static constexpr int ZE = pick_ZE(N, Q, SA, pick_S2(N, Q), 3 * ZC, 9 * Q * pick_S2(N, Q), NT);  // element stride
-  static constexpr int S2 = pick_S2(N, Q);
+  static constexpr int ZE = pick_ZE(N, Q, SA, pick_S2(N, Q, G), 3 * ZC, 9 * Q * pick_S2(N, Q, G), NT, G);  // element stride
+  static constexpr int S2 = pick_S2(N, Q, G);
   static constexpr int YV = Q * S2;        // variant stride (Y0 | Y1 | Y2)
   static constexpr int YC = 3 * YV;        // component stride
-  static constexpr int YE = pick_YE(N, Q, SA, S2, ZE, 3 * YC, NT);  // element stride
-  static constexpr int TAB = (TABSZ + 1) & ~1;  // coefficient tables (B then D, or folded)
+  static constexpr int YE = pick_YE(N, Q, SA, S2, ZE, 3 * YC, NT, G);  // element stride
+  static constexpr int TAB = (TABSZ + AL - 1) & ~(AL - 1);  // coefficient tables (B then D, or folded)
   // elements per CTA: enough x-lines for every thread in stage X; at low order also enough
   // z-columns (N^2 per element) to keep every thread busy in stages Z and Zt.
   static constexpr int EB_lines = (NT / (Q * Q)) > 0 ? NT / (Q * Q) : 1;
   static constexpr int EB_cols = (NT + N * N - 1) / (N * N);
   static constexpr int EB_threads = (ELAS_EB_BY_COLUMNS && EB_cols > EB_lines) ? EB_cols : EB_lines;
-  static constexpr int EB_smem = (kSmemLimit / 8 - TAB) / (ZE + YE);
+  static constexpr int EB_smem = (kSmemLimit / WB - TAB) / (ZE + YE);
   static constexpr int EB = EB_threads < EB_smem ? EB_threads : EB_smem;
-  static constexpr int QDE = qd_stride_lines(Q);             // qdata doubles per element
-  static constexpr int BASE = (TAB + EB * (ZE + YE) + 1) & ~1;  // 16-B aligned start of sQ
+  static constexpr int QDE = qd_stride_words(Q, WB);           // qdata words per element
+  static constexpr int BASE = (TAB + EB * (ZE + YE) + AL - 1) & ~(AL - 1);  // 16-B aligned start of sQ
   // Stage the CTA's quadrature data into shared memory with one TMA bulk copy when two CTAs
   // per SM still fit (latency of the qdata stream then overlaps stages Z and Y).
-  static constexpr bool STAGE_QD = ELAS_QD_STAGING && 8u * (size_t)(BASE + EB * QDE) + 16 <= (size_t)kSmemLimit / 2;
-  static constexpr size_t smem = STAGE_QD ? 8u * (size_t)(BASE + EB * QDE) + 16 : 8u * (size_t)(TAB + EB * (ZE + YE));
+  static constexpr bool STAGE_QD = ELAS_QD_STAGING && (size_t)WB * (size_t)(BASE + EB * QDE) + 16 <= (size_t)kSmemLimit / 2;
+  static constexpr size_t smem = STAGE_QD ? (size_t)WB * (size_t)(BASE + EB * QDE) + 16 : (size_t)WB * (size_t)(TAB + EB * (ZE + YE));
   static_assert(EB >= 1, "element does not fit in shared memory");
 };
 

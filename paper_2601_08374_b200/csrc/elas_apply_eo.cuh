@@ -78,8 +78,8 @@ template <> struct MinbEO<7> { static constexpr int value = ELAS_EO_MINB_P7; };
 template <> struct MinbEO<8> { static constexpr int value = ELAS_EO_MINB_P8; };
 #endif
 
-template <int P, int Q>
-using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEO<P>::value>;
+template <int P, int Q, typename T = double>
+using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEO<P>::value, (int)sizeof(T)>;
 
 // Quadrature-data ring (ELAS_QD_RING = R > 0): every stage-X thread owns one x-line (EB q^2 <=
 // NT), so it streams ITS line's 9 values per point into its own shared-memory slots with
@@ -98,9 +98,10 @@ template <int P> struct StageEO { static constexpr bool value = P != 2; };
 #ifndef ELAS_QD_RING_ALIAS
 #define ELAS_QD_RING_ALIAS 1
 #endif
-template <int P, int Q>
+template <int P, int Q, typename T = double>
 struct RingEO {
-  using C = CfgEO<P, Q>;
+  using C = CfgEO<P, Q, T>;
+  static constexpr int WB = (int)sizeof(T);
   // ALIAS: the ring lives in the Z buffer, idle during stage X (first copies issued after the
   // stage-Y barrier); otherwise it gets its own shared memory and starts at CTA begin.
   static constexpr bool ALIAS = ELAS_QD_RING_ALIAS != 0;
@@ -108,21 +109,45 @@ struct RingEO {
   static constexpr int R0 = ELAS_QD_RING < RMAX ? ELAS_QD_RING : RMAX;
   static constexpr int R = R0 >= 2 ? R0 : 0;
   static constexpr bool STAGE = C::STAGE_QD && R == 0 && StageEO<P>::value;  // whole-CTA TMA staging
-  static constexpr int OFF = ALIAS ? C::TAB : (C::TAB + C::EB * (C::ZE + C::YE) + 1) & ~1;
-  static constexpr size_t smem = (R > 0 && !ALIAS) ? 8u * (size_t)(OFF + R * 9 * C::NT)
-                                 : STAGE ? C::smem : 8u * (size_t)(C::TAB + C::EB * (C::ZE + C::YE));
+  static constexpr int OFF = ALIAS ? C::TAB : (C::TAB + C::EB * (C::ZE + C::YE) + C::AL - 1) & ~(C::AL - 1);
+  static constexpr size_t smem = (R > 0 && !ALIAS) ? (size_t)WB * (size_t)(OFF + R * 9 * C::NT)
+                                 : STAGE ? C::smem : (size_t)WB * (size_t)(C::TAB + C::EB * (C::ZE + C::YE));
 };
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+template <typename T>
+__device__ __forceinline__ void cp_async_w(T* dst, const T* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"((int)sizeof(T)) : "memory");
+}
+
+// sigma~ = r tr(H) I + H + H^T with H = G A~ ; F = sigma~ A~^T (elas_apply.cuh pointwise, any T)
+template <typename T>
+__device__ __forceinline__ void pointwise_t(T (&g)[3][3], const T (&A)[9], T r) {
+  T H[3][3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int m = 0; m < 3; ++m) H[c][m] = fma(g[c][2], A[6 + m], fma(g[c][1], A[3 + m], g[c][0] * A[m]));
+  const T s = r * (H[0][0] + H[1][1] + H[2][2]);
+  T S[3][3];
+  S[0][0] = fma(T(2), H[0][0], s);
+  S[1][1] = fma(T(2), H[1][1], s);
+  S[2][2] = fma(T(2), H[2][2], s);
+  S[0][1] = S[1][0] = H[0][1] + H[1][0];
+  S[0][2] = S[2][0] = H[0][2] + H[2][0];
+  S[1][2] = S[2][1] = H[1][2] + H[2][1];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      g[c][d] = fma(S[c][2], A[3 * d + 2], fma(S[c][1], A[3 * d + 1], S[c][0] * A[3 * d]));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // u (n values per component) -> even (ne) / odd (nh) halves
-template <int N, int NE, int NHX>
-__device__ __forceinline__ void fold_in(const double (&u)[3][N], double (&up)[3][NE], double (&um)[3][NHX]) {
+template <int N, int NE, int NHX, typename T>
+__device__ __forceinline__ void fold_in(const T (&u)[3][N], T (&up)[3][NE], T (&um)[3][NHX]) {
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
 #pragma unroll
@@ -134,23 +159,24 @@ __device__ __forceinline__ void fold_in(const double (&u)[3][N], double (&up)[3]
   }
 }
 
-template <int P, int Q>
-__global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
-    apply_eo_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
-                    const double* __restrict__ rr, const double* __restrict__ tables, Slab s,
+template <int P, int Q, typename T>
+__global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, MinbEO<P>::value)
+    apply_eo_kernel(const double* __restrict__ x, double* __restrict__ y, const T* __restrict__ qd,
+                    const double* __restrict__ rr, const T* __restrict__ tables, Slab s,
                     int64_t e_begin, int64_t e_end, int pref_ctas) {
-  using C = CfgEO<P, Q>;
+  using C = CfgEO<P, Q, T>;
   using F = Fold<P, Q>;
   constexpr int N = C::N, NT = C::NT, EB = C::EB;
   constexpr int NE = F::NE, NH = F::NH, QE = F::QE, QH = F::QH, NHX = F::NHX;
-  using RG = RingEO<P, Q>;
+  using RG = RingEO<P, Q, T>;
   constexpr int R = RG::R;
-  extern __shared__ double smem[];
-  double* tB = smem;            // folded B (parity +1)
-  double* tD = smem + F::TS;    // folded D (parity -1)
-  double* sZ = smem + C::TAB;
-  double* sY = sZ + EB * C::ZE;
-  double* sQ = smem + C::BASE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* smem = reinterpret_cast<T*>(smem_raw);
+  T* tB = smem;            // folded B (parity +1)
+  T* tD = smem + F::TS;    // folded D (parity -1)
+  T* sZ = smem + C::TAB;
+  T* sY = sZ + EB * C::ZE;
+  T* sQ = smem + C::BASE;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + C::BASE + EB * C::QDE);
 
   const int tid = threadIdx.x;
@@ -159,7 +185,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
   if constexpr (RG::STAGE) {
     if (tid == 0) {
       const uint32_t bar = smem_u32(mbar);
-      const uint32_t bytes = (uint32_t)(8 * ne * C::QDE);
+      const uint32_t bytes = (uint32_t)(sizeof(T) * ne * C::QDE);
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
@@ -170,13 +196,13 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
     }
   }
   // this thread's stage-X line (at most one: EB q^2 <= NT) and its qdata ring
-  double* ring = smem + RG::OFF + tid;
+  T* ring = smem + RG::OFF + tid;
   const bool has_line = tid < ne * Q * Q;
-  const double* qline = qd + (e0 + tid / (Q * Q)) * (int64_t)C::QDE + tid % (Q * Q);
+  const T* qline = qd + (e0 + tid / (Q * Q)) * (int64_t)C::QDE + tid % (Q * Q);
   auto ring_issue = [&](int a1) {
     if (has_line) {
 #pragma unroll
-      for (int f = 0; f < 9; ++f) cp_async8(ring + ((a1 % (R > 0 ? R : 1)) * 9 + f) * NT, qline + (a1 * 9 + f) * Q * Q);
+      for (int f = 0; f < 9; ++f) cp_async_w(ring + ((a1 % (R > 0 ? R : 1)) * 9 + f) * NT, qline + (a1 * 9 + f) * Q * Q);
     }
     cp_async_commit();
   };
@@ -192,7 +218,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
   const bool bc = s.faces != 0;
   const bool zcol = tid < ne * N * N;
   const int zi = tid % N, zj = (tid / N) % N, zel = tid / (N * N);
-  double u[3][N];
+  T u[3][N];
   if (zcol) {
     const uint32_t e32 = (uint32_t)(e0 + zel), nx = (uint32_t)s.nx, ny = (uint32_t)s.ny;
     const uint32_t exy = e32 / nx, ex = e32 - exy * nx, ez = exy / ny, ey = exy - ez * ny;
@@ -202,11 +228,11 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
     for (int k = 0; k < N; ++k) {
       const bool cons = bc && is_constrained(I, J, (int)ez * P + k, s);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) u[c][k] = cons ? 0.0 : __ldg(x + c * s.nodes + base + k * plane);
+      for (int c = 0; c < 3; ++c) u[c][k] = cons ? T(0) : (T)__ldg(x + c * s.nodes + base + k * plane);
     }
   }
   {
-    const double* ft = tables + 2 * Q * N;   // fold(B) | fold(D) follow the plain tables
+    const T* ft = tables + 2 * Q * N;   // fold(B) | fold(D) follow the plain tables
     for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = ft[t];
   }
 #if ELAS_L2_PREFETCH
@@ -215,7 +241,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
     if (pe0 < e_end) {
       const int64_t pne = (e_end - pe0) < EB ? (e_end - pe0) : EB;
       const uintptr_t a0 = (uintptr_t)(qd + pe0 * (int64_t)C::QDE);
-      const uintptr_t a1 = a0 + (uintptr_t)(pne * C::QDE * 8);
+      const uintptr_t a1 = a0 + (uintptr_t)(pne * C::QDE * sizeof(T));
       const uintptr_t lo = a0 & ~(uintptr_t)15, hi = (a1 + 15) & ~(uintptr_t)15;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
     }
@@ -226,31 +252,31 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
   // ---------------- Stage Z: folded contraction in z of the gathered column -------------
   if (zcol) {
     const int i = zi, j = zj, el = zel;
-    double up[3][NE], um[3][NHX];
+    T up[3][NE], um[3][NHX];
     fold_in<N, NE, NHX>(u, up, um);
-    double* dst = sZ + el * C::ZE + j * N + i;
+    T* dst = sZ + el * C::ZE + j * N + i;
 #pragma unroll
     for (int a = 0; a < QE; ++a) {
       const bool mid = (Q & 1) && a == QH;
-      double eb[3] = {0, 0, 0}, ob[3] = {0, 0, 0}, ed[3] = {0, 0, 0}, od[3] = {0, 0, 0};
+      T eb[3] = {0, 0, 0}, ob[3] = {0, 0, 0}, ed[3] = {0, 0, 0}, od[3] = {0, 0, 0};
 #pragma unroll
       for (int k = 0; k < NE; ++k) {
-        const double b = tB[F::FE + a * NE + k];
+        const T b = tB[F::FE + a * NE + k];
 #pragma unroll
         for (int c = 0; c < 3; ++c) eb[c] = fma(b, up[c][k], eb[c]);
         if (!mid) {
-          const double d = tD[F::FE + a * NE + k];
+          const T d = tD[F::FE + a * NE + k];
 #pragma unroll
           for (int c = 0; c < 3; ++c) ed[c] = fma(d, up[c][k], ed[c]);
         }
       }
 #pragma unroll
       for (int k = 0; k < NH; ++k) {
-        const double d = tD[F::FO + a * NH + k];
+        const T d = tD[F::FO + a * NH + k];
 #pragma unroll
         for (int c = 0; c < 3; ++c) od[c] = fma(d, um[c][k], od[c]);
         if (!mid) {
-          const double b = tB[F::FO + a * NH + k];
+          const T b = tB[F::FO + a * NH + k];
 #pragma unroll
           for (int c = 0; c < 3; ++c) ob[c] = fma(b, um[c][k], ob[c]);
         }
@@ -271,10 +297,10 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
   // ---------------- Stage Y: folded contraction in y ------------------------------------
   for (int w = tid; w < ne * Q * N; w += NT) {
     const int i = w % N, a3 = (w / N) % Q, el = w / (N * Q);
-    const double* src = sZ + el * C::ZE + a3 * C::SA + i;
-    double bp[3][NE], bm[3][NHX], dp[3][NE], dm[3][NHX];
+    const T* src = sZ + el * C::ZE + a3 * C::SA + i;
+    T bp[3][NE], bm[3][NHX], dp[3][NE], dm[3][NHX];
     {
-      double zb[3][N], zd[3][N];
+      T zb[3][N], zd[3][N];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -285,34 +311,34 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
       fold_in<N, NE, NHX>(zb, bp, bm);
       fold_in<N, NE, NHX>(zd, dp, dm);
     }
-    double* dst = sY + el * C::YE + a3 * N + i;
+    T* dst = sY + el * C::YE + a3 * N + i;
 #pragma unroll
     for (int a2 = 0; a2 < QE; ++a2) {
       const bool mid = (Q & 1) && a2 == QH;
       // y0 = By zb (+1), y1 = Dy zb (-1), y2 = By zd (+1)
-      double e0[3] = {0, 0, 0}, o0[3] = {0, 0, 0}, e1[3] = {0, 0, 0}, o1[3] = {0, 0, 0};
-      double e2[3] = {0, 0, 0}, o2[3] = {0, 0, 0};
+      T e0[3] = {0, 0, 0}, o0[3] = {0, 0, 0}, e1[3] = {0, 0, 0}, o1[3] = {0, 0, 0};
+      T e2[3] = {0, 0, 0}, o2[3] = {0, 0, 0};
 #pragma unroll
       for (int j = 0; j < NE; ++j) {
-        const double b = tB[F::FE + a2 * NE + j];
+        const T b = tB[F::FE + a2 * NE + j];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           e0[c] = fma(b, bp[c][j], e0[c]);
           e2[c] = fma(b, dp[c][j], e2[c]);
         }
         if (!mid) {
-          const double d = tD[F::FE + a2 * NE + j];
+          const T d = tD[F::FE + a2 * NE + j];
 #pragma unroll
           for (int c = 0; c < 3; ++c) e1[c] = fma(d, bp[c][j], e1[c]);
         }
       }
 #pragma unroll
       for (int j = 0; j < NH; ++j) {
-        const double d = tD[F::FO + a2 * NH + j];
+        const T d = tD[F::FO + a2 * NH + j];
 #pragma unroll
         for (int c = 0; c < 3; ++c) o1[c] = fma(d, bm[c][j], o1[c]);
         if (!mid) {
-          const double b = tB[F::FO + a2 * NH + j];
+          const T b = tB[F::FO + a2 * NH + j];
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             o0[c] = fma(b, bm[c][j], o0[c]);
@@ -350,15 +376,15 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
     const int L = w % (Q * Q), el = w / (Q * Q);
     const int a3 = L % Q, a2 = L / Q;
     const int64_t e = e0 + el;
-    double* line = sY + el * C::YE + a2 * C::S2 + a3 * N;
-    double g[3][3][Q];
+    T* line = sY + el * C::YE + a2 * C::S2 + a3 * N;
+    T g[3][3][Q];
 #pragma unroll
     for (int v = 0; v < 3; ++v) {
-      const double* tab = (v == 0) ? tD : tB;   // x-derivative for v = 0 (parity -1)
+      const T* tab = (v == 0) ? tD : tB;   // x-derivative for v = 0 (parity -1)
       const bool odd = (v == 0);
-      double fp[3][NE], fm[3][NHX];
+      T fp[3][NE], fm[3][NHX];
       {
-        double f[3][N];
+        T f[3][N];
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -368,11 +394,11 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
 #pragma unroll
       for (int a1 = 0; a1 < QE; ++a1) {
         const bool mid = (Q & 1) && a1 == QH;
-        double ev[3] = {0, 0, 0}, ov[3] = {0, 0, 0};
+        T ev[3] = {0, 0, 0}, ov[3] = {0, 0, 0};
         if (!(mid && odd)) {
 #pragma unroll
           for (int i = 0; i < NE; ++i) {
-            const double t = tab[F::FE + a1 * NE + i];
+            const T t = tab[F::FE + a1 * NE + i];
 #pragma unroll
             for (int c = 0; c < 3; ++c) ev[c] = fma(t, fp[c][i], ev[c]);
           }
@@ -380,7 +406,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
         if (!(mid && !odd)) {
 #pragma unroll
           for (int i = 0; i < NH; ++i) {
-            const double t = tab[F::FO + a1 * NH + i];
+            const T t = tab[F::FO + a1 * NH + i];
 #pragma unroll
             for (int c = 0; c < 3; ++c) ov[c] = fma(t, fm[c][i], ov[c]);
           }
@@ -392,16 +418,16 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
         }
       }
     }
-    const double r = __ldg(rr + e);
-    const double* qp = RG::STAGE ? sQ + el * C::QDE + L : qd + e * (int64_t)C::QDE + L;
-    double An[9];
+    const T r = (T)__ldg(rr + e);
+    const T* qp = RG::STAGE ? sQ + el * C::QDE + L : qd + e * (int64_t)C::QDE + L;
+    T An[9];
     if constexpr (R == 0) {
 #pragma unroll
       for (int f = 0; f < 9; ++f) An[f] = qp[f * Q * Q];
     }
 #pragma unroll
     for (int a1 = 0; a1 < Q; ++a1) {
-      double A[9];
+      T A[9];
       if constexpr (R > 0) {
         if (a1 + R - 1 < Q) ring_issue(a1 + R - 1);
         else cp_async_commit();                    // empty group keeps the count uniform
@@ -416,12 +442,12 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
           for (int f = 0; f < 9; ++f) An[f] = qp[((a1 + 1) * 9 + f) * Q * Q];
         }
       }
-      double G[3][3];
+      T G[3][3];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int d = 0; d < 3; ++d) G[c][d] = g[c][d][a1];
-      pointwise(G, A, r);
+      pointwise_t<T>(G, A, r);
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -429,25 +455,25 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
     }
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      const double* tab = (d == 0) ? tD : tB;
+      const T* tab = (d == 0) ? tD : tB;
       const bool odd = (d == 0);
       // fold over the points a1 in place: g[.][a] <- g_a + g_{q-1-a}, g[.][q-1-a] <- g_a - g_{q-1-a}
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int a = 0; a < QH; ++a) {
-          const double lo = g[c][d][a], hi = g[c][d][Q - 1 - a];
+          const T lo = g[c][d][a], hi = g[c][d][Q - 1 - a];
           g[c][d][a] = lo + hi;
           g[c][d][Q - 1 - a] = lo - hi;
         }
 #pragma unroll
       for (int i = 0; i < NE; ++i) {
         const bool mid = (N & 1) && i == NH;
-        double ev[3] = {0, 0, 0}, ov[3] = {0, 0, 0};
+        T ev[3] = {0, 0, 0}, ov[3] = {0, 0, 0};
         if (!(mid && odd)) {
 #pragma unroll
           for (int a = 0; a < QE; ++a) {
-            const double t = tab[F::BE + i * QE + a];
+            const T t = tab[F::BE + i * QE + a];
 #pragma unroll
             for (int c = 0; c < 3; ++c) ev[c] = fma(t, g[c][d][a], ev[c]);
           }
@@ -455,7 +481,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
         if (!(mid && !odd)) {
 #pragma unroll
           for (int a = 0; a < QH; ++a) {
-            const double t = tab[F::BO + i * QH + a];
+            const T t = tab[F::BO + i * QH + a];
 #pragma unroll
             for (int c = 0; c < 3; ++c) ov[c] = fma(t, g[c][d][Q - 1 - a], ov[c]);
           }
@@ -473,9 +499,9 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
   // ---------------- Stage Yt: folded transposed contraction in y ------------------------
   for (int w = tid; w < ne * Q * N; w += NT) {
     const int i = w % N, a3 = (w / N) % Q, el = w / (N * Q);
-    const double* src = sY + el * C::YE + a3 * N + i;
+    const T* src = sY + el * C::YE + a3 * N + i;
     // wb = By^T V0 + Dy^T V1, wd = By^T V2 ; X/Y sums per node pair (j, n-1-j)
-    double bX[3][NE], bY[3][NE], dX[3][NE], dY[3][NE];
+    T bX[3][NE], bY[3][NE], dX[3][NE], dY[3][NE];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -483,19 +509,19 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
 #pragma unroll
     for (int a = 0; a < QE; ++a) {
       const bool mid = (Q & 1) && a == QH;
-      double v0p[3], v0m[3], v1p[3], v1m[3], v2p[3], v2m[3];
+      T v0p[3], v0m[3], v1p[3], v1m[3], v2p[3], v2m[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const double l0 = src[c * C::YC + a * C::S2];
-        const double l1 = src[c * C::YC + C::YV + a * C::S2];
-        const double l2 = src[c * C::YC + 2 * C::YV + a * C::S2];
+        const T l0 = src[c * C::YC + a * C::S2];
+        const T l1 = src[c * C::YC + C::YV + a * C::S2];
+        const T l2 = src[c * C::YC + 2 * C::YV + a * C::S2];
         if (mid) {
           v0p[c] = l0; v1p[c] = l1; v2p[c] = l2;
           v0m[c] = v1m[c] = v2m[c] = 0.0;
         } else {
-          const double h0 = src[c * C::YC + (Q - 1 - a) * C::S2];
-          const double h1 = src[c * C::YC + C::YV + (Q - 1 - a) * C::S2];
-          const double h2 = src[c * C::YC + 2 * C::YV + (Q - 1 - a) * C::S2];
+          const T h0 = src[c * C::YC + (Q - 1 - a) * C::S2];
+          const T h1 = src[c * C::YC + C::YV + (Q - 1 - a) * C::S2];
+          const T h2 = src[c * C::YC + 2 * C::YV + (Q - 1 - a) * C::S2];
           v0p[c] = l0 + h0; v0m[c] = l0 - h0;
           v1p[c] = l1 + h1; v1m[c] = l1 - h1;
           v2p[c] = l2 + h2; v2m[c] = l2 - h2;
@@ -504,8 +530,8 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
 #pragma unroll
       for (int j = 0; j < NE; ++j) {
         const bool jmid = (N & 1) && j == NH;
-        const double be = tB[F::BE + j * QE + a];
-        const double de = tD[F::BE + j * QE + a];
+        const T be = tB[F::BE + j * QE + a];
+        const T de = tD[F::BE + j * QE + a];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           bX[c][j] = fma(be, v0p[c], bX[c][j]);
@@ -513,8 +539,8 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
           if (!jmid) bY[c][j] = fma(de, v1p[c], bY[c][j]);
         }
         if (!mid) {
-          const double bo = tB[F::BO + j * QH + a];
-          const double dO = tD[F::BO + j * QH + a];
+          const T bo = tB[F::BO + j * QH + a];
+          const T dO = tD[F::BO + j * QH + a];
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             bX[c][j] = fma(dO, v1m[c], bX[c][j]);
@@ -526,7 +552,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
         }
       }
     }
-    double* dst = sZ + el * C::ZE + a3 * C::SA + i;
+    T* dst = sZ + el * C::ZE + a3 * C::SA + i;
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -548,8 +574,8 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
     const uint32_t e32 = (uint32_t)(e0 + el), nxu = (uint32_t)s.nx, nyu = (uint32_t)s.ny;
     const uint32_t exy = e32 / nxu;
     const int ex = (int)(e32 - exy * nxu), ez = (int)(exy / nyu), ey = (int)(exy - (uint32_t)ez * nyu);
-    const double* src = sZ + el * C::ZE + j * N + i;
-    double X[3][NE], Y[3][NE];
+    const T* src = sZ + el * C::ZE + j * N + i;
+    T X[3][NE], Y[3][NE];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -557,15 +583,15 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
 #pragma unroll
     for (int a = 0; a < QE; ++a) {
       const bool mid = (Q & 1) && a == QH;
-      double wbp[3], wbm[3], wdp[3], wdm[3];
+      T wbp[3], wbm[3], wdp[3], wdm[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const double lb = src[c * C::ZC + a * C::SA], ld = src[c * C::ZC + C::ZV + a * C::SA];
+        const T lb = src[c * C::ZC + a * C::SA], ld = src[c * C::ZC + C::ZV + a * C::SA];
         if (mid) {
           wbp[c] = lb; wdp[c] = ld; wbm[c] = wdm[c] = 0.0;
         } else {
-          const double hb = src[c * C::ZC + (Q - 1 - a) * C::SA];
-          const double hd = src[c * C::ZC + C::ZV + (Q - 1 - a) * C::SA];
+          const T hb = src[c * C::ZC + (Q - 1 - a) * C::SA];
+          const T hd = src[c * C::ZC + C::ZV + (Q - 1 - a) * C::SA];
           wbp[c] = lb + hb; wbm[c] = lb - hb;
           wdp[c] = ld + hd; wdm[c] = ld - hd;
         }
@@ -573,16 +599,16 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
 #pragma unroll
       for (int k = 0; k < NE; ++k) {
         const bool kmid = (N & 1) && k == NH;
-        const double be = tB[F::BE + k * QE + a];
-        const double de = tD[F::BE + k * QE + a];
+        const T be = tB[F::BE + k * QE + a];
+        const T de = tD[F::BE + k * QE + a];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           X[c][k] = fma(be, wbp[c], X[c][k]);
           if (!kmid) Y[c][k] = fma(de, wdp[c], Y[c][k]);
         }
         if (!mid) {
-          const double bo = tB[F::BO + k * QH + a];
-          const double dO = tD[F::BO + k * QH + a];
+          const T bo = tB[F::BO + k * QH + a];
+          const T dO = tD[F::BO + k * QH + a];
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             X[c][k] = fma(dO, wdm[c], X[c][k]);
@@ -598,63 +624,70 @@ __global__ void __launch_bounds__(CfgEO<P, Q>::NT, MinbEO<P>::value)
       const bool kmid = (N & 1) && k == NH;
       if (!(bc && is_constrained(I, J, ez * P + k, s))) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) atomicAdd(y + c * s.nodes + base + k * plane, kmid ? X[c][k] : X[c][k] + Y[c][k]);
+        for (int c = 0; c < 3; ++c) atomicAdd(y + c * s.nodes + base + k * plane, (double)(kmid ? X[c][k] : X[c][k] + Y[c][k]));
       }
       if (!kmid && !(bc && is_constrained(I, J, ez * P + N - 1 - k, s))) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) atomicAdd(y + c * s.nodes + base + (N - 1 - k) * plane, X[c][k] - Y[c][k]);
+        for (int c = 0; c < 3; ++c) atomicAdd(y + c * s.nodes + base + (N - 1 - k) * plane, (double)(X[c][k] - Y[c][k]));
       }
     }
   }
 }
 
-template <int P, int Q>
-cudaError_t launch_apply_eo_pq(const Slab& s, const double* x, double* y, const double* qd, const double* rr,
-                               const double* tables, int64_t e_begin, int64_t e_end, cudaStream_t st) {
-  using C = CfgEO<P, Q>;
+template <int P, int Q, typename T>
+cudaError_t launch_apply_eo_pq(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
+                               const void* tables, int64_t e_begin, int64_t e_end, cudaStream_t st) {
+  using C = CfgEO<P, Q, T>;
+  using RG = RingEO<P, Q, T>;
   static bool attr_done = false;
   static int pref = -1;
   if (!attr_done) {
-    cudaError_t err = cudaFuncSetAttribute(apply_eo_kernel<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)RingEO<P, Q>::smem);
+    cudaError_t err = cudaFuncSetAttribute(apply_eo_kernel<P, Q, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)RG::smem);
     if (err != cudaSuccess) return err;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_eo_kernel<P, Q>, C::NT, RingEO<P, Q>::smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_eo_kernel<P, Q, T>, C::NT, RG::smem);
     pref = sms * (per_sm > 0 ? per_sm : 1);
     attr_done = true;
   }
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
   const int64_t grid = (ne + C::EB - 1) / C::EB;
-  apply_eo_kernel<P, Q><<<(unsigned)grid, C::NT, RingEO<P, Q>::smem, st>>>(x, y, qd, rr, tables, s, e_begin, e_end, pref);
+  apply_eo_kernel<P, Q, T><<<(unsigned)grid, C::NT, RG::smem, st>>>(x, y, static_cast<const T*>(qd), rr,
+                                                                     static_cast<const T*>(tables), s, e_begin,
+                                                                     e_end, pref);
   return cudaGetLastError();
 }
 
-template <int P, int Q>
+template <int P, int Q, typename T>
 void info_eo_pq(ApplyLaunch* info) {
-  using C = CfgEO<P, Q>;
+  using C = CfgEO<P, Q, T>;
   info->threads = C::NT;
   info->elems_per_cta = C::EB;
-  info->smem_bytes = RingEO<P, Q>::smem;
+  info->smem_bytes = RingEO<P, Q, T>::smem;
 }
 
 }  // namespace elas
 
 #define ELAS_DEFINE_DEGREE_EO(P)                                                                \
   namespace elas {                                                                              \
-  cudaError_t apply_eo_info_p##P(int q, ApplyLaunch* info) {                                    \
-    if (q == P + 1) info_eo_pq<P, P + 1>(info);                                                 \
-    else if (q == P + 2) info_eo_pq<P, P + 2>(info);                                            \
+  cudaError_t apply_eo_info_p##P(int q, int fp32, ApplyLaunch* info) {                          \
+    if (q == P + 1) fp32 ? info_eo_pq<P, P + 1, float>(info) : info_eo_pq<P, P + 1, double>(info); \
+    else if (q == P + 2) fp32 ? info_eo_pq<P, P + 2, float>(info) : info_eo_pq<P, P + 2, double>(info); \
     else return cudaErrorInvalidValue;                                                          \
     return cudaSuccess;                                                                         \
   }                                                                                             \
-  cudaError_t apply_eo_launch_p##P(int q, const Slab& s, const double* x, double* y,            \
-                                   const double* qd, const double* rr, const double* tables,    \
+  cudaError_t apply_eo_launch_p##P(int q, int fp32, const Slab& s, const double* x, double* y,  \
+                                   const void* qd, const double* rr, const void* tables,        \
                                    int64_t e_begin, int64_t e_end, cudaStream_t st) {           \
-    if (q == P + 1) return launch_apply_eo_pq<P, P + 1>(s, x, y, qd, rr, tables, e_begin, e_end, st); \
-    if (q == P + 2) return launch_apply_eo_pq<P, P + 2>(s, x, y, qd, rr, tables, e_begin, e_end, st); \
+    if (q == P + 1)                                                                             \
+      return fp32 ? launch_apply_eo_pq<P, P + 1, float>(s, x, y, qd, rr, tables, e_begin, e_end, st) \
+                  : launch_apply_eo_pq<P, P + 1, double>(s, x, y, qd, rr, tables, e_begin, e_end, st); \
+    if (q == P + 2)                                                                             \
+      return fp32 ? launch_apply_eo_pq<P, P + 2, float>(s, x, y, qd, rr, tables, e_begin, e_end, st) \
+                  : launch_apply_eo_pq<P, P + 2, double>(s, x, y, qd, rr, tables, e_begin, e_end, st); \
     return cudaErrorInvalidValue;                                                               \
   }                                                                                             \
   }

@@ -30,10 +30,11 @@ int host_tables(int p, int q, double* nodes, double* points, double* weights, do
 int fold_table_size(int p, int q);
 void host_fold_table(int p, int q, const double* T, double* out);
 
-// folded-SIMT variant (elas_apply_eo_p<P>.cu)
-cudaError_t apply_eo_info(int p, int q, ApplyLaunch* info);
-cudaError_t apply_eo_launch(int p, int q, const Slab& s, const double* x, double* y, const double* qd,
-                            const double* rr, const double* tables, int64_t e_begin, int64_t e_end,
+// folded-SIMT variant (elas_apply_eo_p<P>.cu); fp32 != 0: the mixed-precision instance (FP32
+// qdata, tables and arithmetic; FP64 x, y and scatter)
+cudaError_t apply_eo_info(int p, int q, int fp32, ApplyLaunch* info);
+cudaError_t apply_eo_launch(int p, int q, int fp32, const Slab& s, const double* x, double* y, const void* qd,
+                            const double* rr, const void* tables, int64_t e_begin, int64_t e_end,
                             cudaStream_t st);
 
 // Per-degree translation units (elas_apply_p<P>.cu) export these; q must be p+1 or p+2.
@@ -52,12 +53,16 @@ cudaError_t apply_tc_launch(const Slab& s, const double* x, double* y, const dou
 // kernel: qd[e][slice a1/2][r][f][lane], r = 2 (a1 % 2) + a3 % 2, lane = 4 a2 + a3 / 2.
 // 2 = lane-interleaved blocks of 32 elements for the one-thread-per-element p = 1 kernel:
 //     qd[e / 32][pt][f][e % 32], pt = a1 + q (a2 + q a3).
-enum { QD_LAYOUT_LINES = 0, QD_LAYOUT_TC6 = 1, QD_LAYOUT_E32 = 2 };
+// 3 = layout 0 in FP32 words (mixed-precision folded kernel), element stride rounded to 4 floats.
+enum { QD_LAYOUT_LINES = 0, QD_LAYOUT_TC6 = 1, QD_LAYOUT_E32 = 2, QD_LAYOUT_LINES_F32 = 3 };
 
 // qdata doubles per element: 9 q^3 rounded up to even so every element starts 16-B aligned
 // (TMA bulk copies need 16-B aligned addresses and sizes).
 constexpr int qd_stride_lines(int q) { return (9 * q * q * q + 1) & ~1; }
-inline int qd_stride(int q, int layout) { return layout == QD_LAYOUT_LINES ? qd_stride_lines(q) : 9 * q * q * q; }
+inline int qd_stride(int q, int layout) {
+  return layout == QD_LAYOUT_LINES ? qd_stride_lines(q) : layout == QD_LAYOUT_LINES_F32 ? (9 * q * q * q + 3) & ~3 : 9 * q * q * q;
+}
+inline size_t qd_word_bytes(int layout) { return layout == QD_LAYOUT_LINES_F32 ? 4 : 8; }
 // elements the qdata allocation must cover (E32 pads to whole blocks of 32)
 inline int64_t qd_elems(int64_t ne, int layout) { return layout == QD_LAYOUT_E32 ? (ne + 31) / 32 * 32 : ne; }
 

@@ -16,7 +16,8 @@ struct elas_op {
   bool external = false;            // nranks > 1 without a communicator
   double* qd = nullptr;             // 9 q^3 doubles per element
   double* rr = nullptr;             // lambda/mu per element
-  double* tab = nullptr;            // B then D (q x (p+1) each)
+  double* tab = nullptr;            // B | D | fold(B) | fold(D)
+  float* tabf = nullptr;            // FP32 copy of tab (mixed-precision folded kernel)
   double* xs = nullptr;             // staging for elas_apply_host
   double* ys = nullptr;
   cudaStream_t stream = nullptr;

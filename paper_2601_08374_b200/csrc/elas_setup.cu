@@ -81,6 +81,12 @@ __global__ void qdata_kernel(int q, int layout, Slab s, const double* __restrict
       double* out = qd + e * (int64_t)(9 * q3) + (int64_t)((sl * 4 + r) * 9) * 32 + lane;
       for (int d = 0; d < 3; ++d)
         for (int m = 0; m < 3; ++m) out[(3 * d + m) * 32] = sc * adj[d][m];
+    } else if (layout == QD_LAYOUT_LINES_F32) {   // mixed precision: the same values rounded to FP32
+      const int L = a3 + q * a2;
+      float* out = reinterpret_cast<float*>(qd) + e * (int64_t)((9 * q3 + 3) & ~3) +
+                   (int64_t)a1 * 9 * q * q + L;
+      for (int d = 0; d < 3; ++d)
+        for (int m = 0; m < 3; ++m) out[(3 * d + m) * q * q] = (float)(sc * adj[d][m]);
     } else {
       const int L = a3 + q * a2;
       double* out = qd + e * (int64_t)qd_stride_lines(q) + (int64_t)a1 * 9 * q * q + L;

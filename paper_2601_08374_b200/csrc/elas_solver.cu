@@ -61,22 +61,23 @@ __device__ __forceinline__ bool cons_node(int64_t node, const Slab& s) {
 
 // ------------------------------------------------------------------------- diagonal
 
-// pointer to A~[f] (f = 3 k + m) at point (a1, a2, a3) of element e, for every qdata layout
-__device__ __forceinline__ const double* qd_point(const double* qd, int layout, int q, int64_t e, int a1, int a2,
-                                                  int a3, int& fstride) {
+// word offset of A~[0] (f = 3 k + m at + f * fstride) at point (a1, a2, a3) of element e, for
+// every qdata layout (QD_LAYOUT_LINES_F32 holds floats; the caller reads accordingly)
+__device__ __forceinline__ int64_t qd_offset(int layout, int q, int64_t e, int a1, int a2, int a3, int& fstride) {
   const int q3 = q * q * q;
   if (layout == QD_LAYOUT_E32) {
     fstride = 32;
     const int pt = a1 + q * (a2 + q * a3);
-    return qd + (e >> 5) * (int64_t)(32 * 9 * q3) + (int64_t)pt * 9 * 32 + (e & 31);
+    return (e >> 5) * (int64_t)(32 * 9 * q3) + (int64_t)pt * 9 * 32 + (e & 31);
   }
   if (layout == QD_LAYOUT_TC6) {
     fstride = 32;
     const int sl = a1 >> 1, r = 2 * (a1 & 1) + (a3 & 1), lane = 4 * a2 + (a3 >> 1);
-    return qd + e * (int64_t)(9 * q3) + (int64_t)((sl * 4 + r) * 9) * 32 + lane;
+    return e * (int64_t)(9 * q3) + (int64_t)((sl * 4 + r) * 9) * 32 + lane;
   }
   fstride = q * q;
-  return qd + e * (int64_t)qd_stride_lines(q) + (int64_t)a1 * 9 * q * q + a3 + q * a2;
+  const int64_t es = layout == QD_LAYOUT_LINES_F32 ? (int64_t)((9 * q3 + 3) & ~3) : (int64_t)qd_stride_lines(q);
+  return e * es + (int64_t)a1 * 9 * q * q + a3 + q * a2;
 }
 
 __global__ void diag_init_kernel(Slab s, double* __restrict__ d) {
@@ -117,11 +118,14 @@ __global__ void __launch_bounds__(128) diag_kernel(int p, int q, int layout, Sla
     for (int pt = tid; pt < q3; pt += NT) {
       const int a1 = pt % q, a2 = (pt / q) % q, a3 = pt / (q * q);
       int fs;
-      const double* A = qd_point(qd, layout, q, e, a1, a2, a3, fs);
+      const int64_t off = qd_offset(layout, q, e, a1, a2, a3, fs);
+      const float* qf = reinterpret_cast<const float*>(qd);
+      const bool f32 = layout == QD_LAYOUT_LINES_F32;
       double Ak[3], Al[3];
       for (int m = 0; m < 3; ++m) {
-        Ak[m] = A[(3 * k + m) * fs];
-        Al[m] = A[(3 * l + m) * fs];
+        const int64_t ik = off + (3 * k + m) * fs, il = off + (3 * l + m) * fs;
+        Ak[m] = f32 ? (double)qf[ik] : qd[ik];
+        Al[m] = f32 ? (double)qf[il] : qd[il];
       }
       const double dot = Ak[0] * Al[0] + Ak[1] * Al[1] + Ak[2] * Al[2];
       for (int c = 0; c < 3; ++c) T0[c * q3 + pt] = r1 * Ak[c] * Al[c] + dot;
@@ -472,8 +476,11 @@ int elas_pcg(elas_op* op, int precond, elas_cheb* cheb, const double* b, double*
              elas_solve_report* rep, double* history) {
   if (!op || !b || !x) { elas::set_error("elas_pcg: NULL argument"); return ELAS_EINVAL; }
   if (!elas::solver_ok(op, "elas_pcg")) return ELAS_EINVAL;
-  if (precond < ELAS_PC_NONE || precond > ELAS_PC_CHEBYSHEV || (precond == ELAS_PC_CHEBYSHEV && (!cheb || cheb->op != op))) {
-    elas::set_error("elas_pcg: unknown preconditioner, or a Chebyshev preconditioner of another operator");
+  if (precond < ELAS_PC_NONE || precond > ELAS_PC_CHEBYSHEV ||
+      (precond == ELAS_PC_CHEBYSHEV && (!cheb || cheb->op->slab.nodes != op->slab.nodes ||
+                                        cheb->op->stream != op->stream))) {
+    elas::set_error("elas_pcg: unknown preconditioner, or a Chebyshev preconditioner whose operator has another "
+                    "vector length or stream");
     return ELAS_EINVAL;
   }
   if (b == x || maxit < 0 || !(rtol >= 0.0)) { elas::set_error("elas_pcg: need b != x, maxit >= 0, rtol >= 0"); return ELAS_EINVAL; }

@@ -390,3 +390,36 @@ def test_folded_agrees_with_simt(cfg):
         ys.append(gpu_apply(P, op=op))
         op.close()
     assert rel_l2(ys[1], ys[0]) <= 1e-14
+
+
+# ---------------------------------------------------------------------------------------
+# mixed precision (FP32 qdata + arithmetic, FP64 vectors and scatter): NOT the 1e-12 contract
+# ---------------------------------------------------------------------------------------
+
+TOL_F32 = 1e-5   # FP32 unit roundoff 6e-8 x O(10-100) accumulated terms
+
+
+@pytest.mark.parametrize("p", range(1, 9))
+@pytest.mark.parametrize("dq", [1, 2])
+def test_folded_f32_vs_oracle(p, dq):
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator, VARIANT_FOLDED_F32
+    P = synth.make_problem("t", 3, 2, 3, p, p + dq, perturb=True, lognormal_material=True,
+                           faces=1 | 8 | 16, seed=400 + 10 * p + dq)
+    op = Operator.from_problem(P, variant=VARIANT_FOLDED_F32)
+    assert op.variant == VARIANT_FOLDED_F32
+    y = gpu_apply(P, op=op)
+    op.close()
+    err = rel_l2(y, oracle.apply(oracle_mesh(P), P.x))
+    assert 1e-12 < err <= TOL_F32          # genuinely FP32 (not silently FP64), within the bound
+
+
+def test_folded_f32_config4_sampled():
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator, VARIANT_FOLDED_F32
+    P = synth.make_config(4, 6)
+    op = Operator.from_problem(P, variant=VARIANT_FOLDED_F32)
+    y = gpu_apply(P, op=op)
+    op.close()
+    rows = sample_rows(P, 128, 6)
+    assert rel_l2(y[rows], oracle.apply_rows(oracle_mesh(P), P.x, rows)) <= TOL_F32

@@ -208,3 +208,27 @@ def test_solver_error_paths():
         op2.chebyshev()
     op2.close()
     op.close()
+
+
+def test_pcg_fp64_with_fp32_chebyshev():
+    """Mixed precision in the solver: FP64 PCG (FP64 operator) preconditioned by a Chebyshev
+    smoother built on the FP32 operator of the same mesh converges to the FP64 tolerance."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator, PC_CHEBYSHEV, VARIANT_FOLDED_F32
+    P = small_problem(4, faces=1, seed=61, dims=(4, 4, 4))
+    n = P.num_dofs
+    op = Operator.from_problem(P)
+    op32 = Operator.from_problem(P, variant=VARIANT_FOLDED_F32)
+    ch64 = op.chebyshev(power_iters=10, seed=3)
+    ch32 = op32.chebyshev(power_iters=10, seed=3)
+    assert abs(ch32.lambda_max - ch64.lambda_max) <= 1e-5 * ch64.lambda_max
+    b = torch.from_numpy(synth.splitmix_uniform(n, 10)).cuda()
+    x = torch.empty_like(b)
+    it64, c64, _, _ = op.pcg(b, x, precond=PC_CHEBYSHEV, cheb=ch64, rtol=1e-10, maxit=3000)
+    it32, c32, r32, _ = op.pcg(b, x, precond=PC_CHEBYSHEV, cheb=ch32, rtol=1e-10, maxit=3000)
+    assert c64 and c32 and r32 <= 1e-10
+    assert it32 <= int(1.2 * it64) + 2
+    Ax = torch.empty_like(b)
+    op.apply(x, Ax)
+    assert float(torch.linalg.norm(Ax - b) / torch.linalg.norm(b)) <= 1e-7
+    ch32.close(); ch64.close(); op32.close(); op.close()
