@@ -279,16 +279,24 @@ def solver_bench(cfg=3, passes=10, rtol=1e-8, maxit=4000):
            "lambda_max": round(ch.lambda_max, 6), "setup_s_diag_plus_10_power_its": round(setup, 4),
            "ms_per_pass": round(pass_ms, 4), "applies_per_pass": 3,
            "gdofs_per_apply_equiv": round(3 * n / (pass_ms / 1e3) / 1e9, 3)}}
-    for name, pc in (("pcg_chebyshev", PC_CHEBYSHEV), ("pcg_jacobi", PC_JACOBI)):
-        op.pcg(b, x, precond=pc, cheb=ch, rtol=rtol, maxit=3)   # warm
+    from paper_2601_08374_b200.elas import VARIANT_FOLDED_F32
+    op32 = Operator.from_problem(P, variant=VARIANT_FOLDED_F32)
+    ch32 = op32.chebyshev(order=3, alpha=0.1, beta=1.1, power_iters=10, seed=1)
+    for name, pc, c in (("pcg_chebyshev", PC_CHEBYSHEV, ch), ("pcg_chebyshev_fp32_smoother", PC_CHEBYSHEV, ch32),
+                        ("pcg_jacobi", PC_JACOBI, None)):
+        op.pcg(b, x, precond=pc, cheb=c, rtol=rtol, maxit=3)   # warm
         torch.cuda.synchronize()
         t = time.perf_counter()
-        it, conv, rel, _ = op.pcg(b, x, precond=pc, cheb=ch, rtol=rtol, maxit=maxit)
+        it, conv, rel, _ = op.pcg(b, x, precond=pc, cheb=c, rtol=rtol, maxit=maxit)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t
         out[name] = {"rtol": rtol, "iterations": it, "converged": conv, "rel_residual": rel,
                      "solve_s": round(dt, 4), "ms_per_iteration": round(dt / max(it, 1) * 1e3, 4),
                      "solver_mdofs": round(n * it / dt / 1e6, 1)}
+    out["pcg_chebyshev_fp32_smoother"]["note"] = ("FP64 CG and operator; the Chebyshev preconditioner runs the "
+                                                  "mixed-precision (FP32) operator of the same mesh")
+    ch32.close()
+    op32.close()
     ch.close()
     op.close()
     torch.cuda.empty_cache()
