@@ -38,3 +38,4 @@ from .elasticity import (  # noqa: F401
     node_coordinates,
 )
 from .solvers import diagonal, power_lambda_max, chebyshev, pcg  # noqa: F401
+from . import gmg  # noqa: F401
