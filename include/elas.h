@@ -204,6 +204,36 @@ typedef struct {
 int elas_pcg(elas_op* op, int precond, elas_cheb* cheb, const double* b, double* x, double rtol, int maxit,
              elas_solve_report* report, double* history);
 
+/* Geometric multigrid V-cycle (Sec. 3, Fig. 2),
+ * single-GPU (nranks == 1).  Readings R22-R25 in DESIGN.md.
+ * create: builds `levels` levels from `fine` (same p, q; h-coarsening by 2 per axis: nx, ny, nz
+ *   divisible by 2^(levels-1); coarse vertices = fine vertices of even index; per-element
+ *   lambda, mu averaged over the 8 children; same Dirichlet faces), each an elas_op of kernel
+ *   `variant` (ELAS_VARIANT_AUTO or any variant valid for (p, q)) with a Chebyshev smoother
+ *   (order, alpha, beta, power_iters, seed as elas_cheb_create).  Transfers: FE interpolation
+ *   in reference coordinates (Kronecker product of 1D interpolations) and its transpose.
+ *   Coarsest level: PCG preconditioned by its Chebyshev smoother, to coarse_rtol (> 0:
+ *   synchronising convergence test) or exactly coarse_maxit iterations (coarse_rtol <= 0: no
+ *   host round trip).  Host arrays are copied.  NULL + message on error.
+ * apply: one V-cycle x = M b (x overwritten; pre- and post-smoothing with the same Chebyshev
+ *   polynomial, so M is symmetric).  DEVICE b, x of the finest level's length; asynchronous.
+ * level_op: the op of level l (0 = finest), owned by the gmg (do not destroy).
+ * pcg_gmg: elas_pcg with the V-cycle as preconditioner (op: typically elas_gmg_level_op(g, 0)). */
+typedef struct elas_gmg elas_gmg;
+elas_gmg* elas_gmg_create(const elas_mesh* fine, int p, int q, const double* lambda, const double* mu, int levels,
+                          int order, double alpha, double beta, int power_iters, unsigned long long seed,
+                          double coarse_rtol, int coarse_maxit, int variant);
+elas_op* elas_gmg_level_op(elas_gmg* g, int level);
+int elas_gmg_levels(const elas_gmg* g);
+int elas_gmg_set_stream(elas_gmg* g, void* cuda_stream);
+int elas_gmg_apply(elas_gmg* g, const double* b, double* x);
+/* The transfers alone: restrict_ = 0: out (level) = P in (level+1); restrict_ = 1: out (level+1)
+ * = P^T in (level), constrained coarse entries zeroed.  0 <= level < levels - 1. */
+int elas_gmg_transfer(elas_gmg* g, int level, int restrict_, const double* in, double* out);
+int elas_pcg_gmg(elas_op* op, elas_gmg* g, const double* b, double* x, double rtol, int maxit,
+                 elas_solve_report* report, double* history);
+void elas_gmg_destroy(elas_gmg* g);   /* NULL-safe; synchronises */
+
 /* Thread-local message describing the last error on this thread ("" if none). */
 const char* elas_last_error(void);
 

@@ -29,6 +29,8 @@ int host_tables(int p, int q, double* nodes, double* points, double* weights, do
 // Even-odd folded copy of one table (elas_tables.cpp); op tables = B | D | fold(B) | fold(D).
 int fold_table_size(int p, int q);
 void host_fold_table(int p, int q, const double* T, double* out);
+// GMG 1D prolongation from a coarse element to its two children, (2p+1) x (p+1) (elas_tables.cpp)
+int host_prolongation_1d(int p, double* M);
 
 // folded-SIMT variant (elas_apply_eo_p<P>.cu); fp32 != 0: the mixed-precision instance (FP32
 // qdata, tables and arithmetic; FP64 x, y and scatter)

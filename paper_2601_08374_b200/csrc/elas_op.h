@@ -39,8 +39,25 @@ struct elas_op {
 };
 
 
+struct elas_cheb {
+  elas_op* op = nullptr;
+  int order = 3;
+  double alpha = 0.1, beta = 1.1, lam_max = 0.0;
+  double* buf = nullptr;   // r, dv, t (3 vectors)
+};
+
+#include <functional>
+
 namespace elas {
 void free_solver_state(elas_op* op);
+// solver internals shared with elas_gmg.cu (elas_solver.cu)
+using PrecondFn = std::function<int(const double* r, double* z)>;
+constexpr int PC_CALLBACK = 100;
+int cheb_run(elas_cheb* ch, const double* b, double* x, bool x_zero);
+// PCG from x = 0; kind: ELAS_PC_NONE / ELAS_PC_JACOBI / PC_CALLBACK (M).  check = false: exactly
+// maxit iterations with no host synchronisation (a fixed-length inner solve).
+int pcg_core(elas_op* op, int kind, const PrecondFn& M, const double* b, double* x, double rtol, int maxit,
+             bool check, elas_solve_report* rep, double* history);
 // exchange the partial interface planes of y with the neighbour ranks and add them (NCCL mode,
 // synchronous on the op's stream); no-op for nranks == 1 or external mode
 int exchange_planes(elas_op* op, double* y);

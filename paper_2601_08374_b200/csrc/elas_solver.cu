@@ -258,7 +258,7 @@ __global__ void cheb_step_kernel(const double* __restrict__ Ad, const double* __
 __global__ void pcg_update_kernel(double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
                                   const double* __restrict__ p, const double* __restrict__ t_,
                                   const double* __restrict__ dinv, const double* __restrict__ S, int64_t n) {
-  const double alpha = S[S_RZ] / S[S_PT];
+  const double alpha = S[S_PT] != 0.0 ? S[S_RZ] / S[S_PT] : 0.0;   // 0/0 only for b = 0 or exact convergence
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     x[t] = fma(alpha, p[t], x[t]);
     const double rt = fma(-alpha, t_[t], r[t]);
@@ -270,7 +270,7 @@ __global__ void pcg_update_kernel(double* __restrict__ x, double* __restrict__ r
 // PCG: beta = S[RZNEW] / S[RZ]; p = z + beta p; then S[RZ] = S[RZNEW] (one thread, after use)
 __global__ void pcg_direction_kernel(double* __restrict__ p, const double* __restrict__ z, double* __restrict__ S,
                                      int64_t n, int first) {
-  const double beta = first ? 0.0 : S[S_RZNEW] / S[S_RZ];
+  const double beta = (first || S[S_RZ] == 0.0) ? 0.0 : S[S_RZNEW] / S[S_RZ];
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
     p[t] = first ? z[t] : fma(beta, p[t], z[t]);
 }
@@ -313,12 +313,6 @@ void free_solver_state(elas_op* op) {
 
 }  // namespace elas
 
-struct elas_cheb {
-  elas_op* op = nullptr;
-  int order = 3;
-  double alpha = 0.1, beta = 1.1, lam_max = 0.0;
-  double* buf = nullptr;   // r, dv, t (3 vectors)
-};
 
 namespace elas {
 namespace {
@@ -361,6 +355,8 @@ bool solver_ok(const elas_op* op, const char* who) {
   return true;
 }
 
+}  // namespace
+
 // x <- x + p_k(D^{-1}A) D^{-1}(b - A x); x_zero: treat x as 0 on entry (preconditioner form)
 int cheb_run(elas_cheb* ch, const double* b, double* x, bool x_zero) {
   elas_op* op = ch->op;
@@ -391,7 +387,72 @@ int cheb_run(elas_cheb* ch, const double* b, double* x, bool x_zero) {
   return ELAS_OK;
 }
 
-}  // namespace
+int pcg_core(elas_op* op, int kind, const PrecondFn& M, const double* b, double* x, double rtol, int maxit,
+             bool check, elas_solve_report* rep, double* history) {
+  int rc;
+  if ((rc = ensure_red(op))) return rc;
+  if (kind == ELAS_PC_JACOBI && (rc = ensure_dinv(op))) return rc;
+  const int64_t n = 3 * op->slab.nodes;
+  if (!op->work) CK(cudaMalloc(&op->work, sizeof(double) * 4 * n), "cudaMalloc (pcg work vectors)");
+  double* r = op->work;
+  double* z = r + n;
+  double* p = z + n;
+  double* t = p + n;
+  cudaStream_t st = op->stream;
+  const int g = grid_for(n);
+  double* S = op->red + RED_BLOCKS;
+  const bool fused_z = kind != PC_CALLBACK;
+  // x = 0, r = b, z = M r
+  CK(cudaMemsetAsync(x, 0, sizeof(double) * n, st), "cudaMemsetAsync");
+  CK(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
+  if (kind == PC_CALLBACK) {
+    if ((rc = M(r, z))) return rc;
+  } else if (kind == ELAS_PC_JACOBI) {
+    scale_kernel<<<g, 256, 0, st>>>(z, op->dinv, r, n);
+  } else {
+    CK(cudaMemcpyAsync(z, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
+  }
+  CK(cudaGetLastError(), "preconditioner kernel");
+  if ((rc = dot(r, z, n, op->red, S_RZ, st))) return rc;
+  double rz0 = 1.0;
+  if (check) {
+    if ((rc = read_scalar(op, S_RZ, &rz0))) return rc;
+    if (rz0 < 0.0 || !std::isfinite(rz0)) { set_error("elas_pcg: preconditioner not positive definite"); return ELAS_EINVAL; }
+  }
+  int it = 0;
+  double rel = rz0 > 0.0 ? 1.0 : 0.0;
+  if (history) history[0] = rel;
+  if (rz0 > 0.0) {
+    pcg_direction_kernel<<<g, 256, 0, st>>>(p, z, S, n, 1);
+    while (it < maxit) {
+      if ((rc = elas_apply(op, p, t))) return rc;
+      if ((rc = dot(p, t, n, op->red, S_PT, st))) return rc;
+      pcg_update_kernel<<<g, 256, 0, st>>>(x, r, fused_z ? z : nullptr, p, t,
+                                           kind == ELAS_PC_JACOBI ? op->dinv : nullptr, S, n);
+      CK(cudaGetLastError(), "pcg update kernel");
+      if (!fused_z && (rc = M(r, z))) return rc;
+      if ((rc = dot(r, z, n, op->red, S_RZNEW, st))) return rc;
+      ++it;
+      if (check) {
+        double rz = 0.0;
+        if ((rc = read_scalar(op, S_RZNEW, &rz))) return rc;
+        rel = std::sqrt(rz > 0.0 ? rz / rz0 : 0.0);
+        if (history) history[it] = rel;
+        if (rel <= rtol) break;
+      }
+      pcg_direction_kernel<<<g, 256, 0, st>>>(p, z, S, n, 0);
+      copy_scalar_kernel<<<1, 1, 0, st>>>(S, S_RZ, S_RZNEW);
+      CK(cudaGetLastError(), "pcg direction kernels");
+    }
+  }
+  if (rep) {
+    rep->iterations = it;
+    rep->rel_residual = check ? rel : -1.0;
+    rep->converged = (check && rel <= rtol) ? 1 : 0;
+  }
+  return ELAS_OK;
+}
+
 }  // namespace elas
 
 using elas::Slab;
@@ -484,64 +545,11 @@ int elas_pcg(elas_op* op, int precond, elas_cheb* cheb, const double* b, double*
     return ELAS_EINVAL;
   }
   if (b == x || maxit < 0 || !(rtol >= 0.0)) { elas::set_error("elas_pcg: need b != x, maxit >= 0, rtol >= 0"); return ELAS_EINVAL; }
-  int rc;
-  if ((rc = elas::ensure_red(op))) return rc;
-  if (precond == ELAS_PC_JACOBI && (rc = elas::ensure_dinv(op))) return rc;
-  const int64_t n = 3 * op->slab.nodes;
-  if (!op->work) CK_C(cudaMalloc(&op->work, sizeof(double) * 4 * n), "cudaMalloc (pcg work vectors)");
-  double* r = op->work;
-  double* z = r + n;
-  double* p = z + n;
-  double* t = p + n;
-  cudaStream_t st = op->stream;
-  const int g = elas::grid_for(n);
-  double* S = op->red + elas::RED_BLOCKS;
-  // x = 0, r = b, z = M r
-  CK_C(cudaMemsetAsync(x, 0, sizeof(double) * n, st), "cudaMemsetAsync");
-  CK_C(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
-  auto precondition = [&]() -> int {
-    if (precond == ELAS_PC_CHEBYSHEV) return elas::cheb_run(cheb, r, z, true);
-    if (precond == ELAS_PC_JACOBI) elas::scale_kernel<<<g, 256, 0, st>>>(z, op->dinv, r, n);
-    else CK_C(cudaMemcpyAsync(z, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
-    CK_C(cudaGetLastError(), "preconditioner kernel");
-    return ELAS_OK;
-  };
-  if ((rc = precondition())) return rc;
-  if ((rc = elas::dot(r, z, n, op->red, elas::S_RZ, st))) return rc;
-  double rz0 = 0.0;
-  if ((rc = elas::read_scalar(op, elas::S_RZ, &rz0))) return rc;
-  int it = 0;
-  double rel = rz0 > 0.0 ? 1.0 : 0.0;
-  if (history && maxit >= 0) history[0] = rel;
-  if (rz0 < 0.0 || !std::isfinite(rz0)) { elas::set_error("elas_pcg: preconditioner not positive definite"); return ELAS_EINVAL; }
-  if (rz0 > 0.0) {
-    elas::pcg_direction_kernel<<<g, 256, 0, st>>>(p, z, S, n, 1);
-    while (it < maxit) {
-      if ((rc = elas_apply(op, p, t))) return rc;
-      if ((rc = elas::dot(p, t, n, op->red, elas::S_PT, st))) return rc;
-      const bool fused_z = precond != ELAS_PC_CHEBYSHEV;
-      elas::pcg_update_kernel<<<g, 256, 0, st>>>(x, r, fused_z ? z : nullptr, p, t,
-                                                 precond == ELAS_PC_JACOBI ? op->dinv : nullptr, S, n);
-      CK_C(cudaGetLastError(), "pcg update kernel");
-      if (!fused_z && (rc = elas::cheb_run(cheb, r, z, true))) return rc;
-      if ((rc = elas::dot(r, z, n, op->red, elas::S_RZNEW, st))) return rc;
-      double rz = 0.0;
-      if ((rc = elas::read_scalar(op, elas::S_RZNEW, &rz))) return rc;
-      ++it;
-      rel = std::sqrt(rz > 0.0 ? rz / rz0 : 0.0);
-      if (history) history[it] = rel;
-      if (rel <= rtol) break;
-      elas::pcg_direction_kernel<<<g, 256, 0, st>>>(p, z, S, n, 0);
-      elas::copy_scalar_kernel<<<1, 1, 0, st>>>(S, elas::S_RZ, elas::S_RZNEW);
-      CK_C(cudaGetLastError(), "pcg direction kernels");
-    }
-  }
-  if (rep) {
-    rep->iterations = it;
-    rep->rel_residual = rel;
-    rep->converged = rel <= rtol ? 1 : 0;
-  }
-  return ELAS_OK;
+  if (precond == ELAS_PC_CHEBYSHEV)
+    return elas::pcg_core(op, elas::PC_CALLBACK,
+                          [cheb](const double* r, double* z) { return elas::cheb_run(cheb, r, z, true); }, b, x,
+                          rtol, maxit, true, rep, history);
+  return elas::pcg_core(op, precond, elas::PrecondFn(), b, x, rtol, maxit, true, rep, history);
 }
 
 }  // extern "C"

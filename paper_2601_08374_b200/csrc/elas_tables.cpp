@@ -177,4 +177,34 @@ void host_fold_table(int p, int q, const double* T, double* out) {
   }
 }
 
+// 1D finite element interpolation from a coarse element to its two children (GMG prolongation,
+// DESIGN.md reading R23): M[t][i] = l_i(xi_c(t)), t = 0 .. 2p indexes the 2p+1 fine GLL nodes of
+// the two children, xi_c(t) = (s + xi_{t - s p}) / 2 with s = (t >= p); barycentric Lagrange on
+// the coarse GLL nodes (exact at coincident nodes).  M has (2p+1) x (p+1) doubles.
+int host_prolongation_1d(int p, double* M) {
+  if (p < 1 || p > 8) return ELAS_EINVAL;
+  const int n = p + 1;
+  std::vector<double> xi(n), bw(n);
+  gll_nodes(p, xi.data());
+  for (int i = 0; i < n; ++i) {
+    double prod = 1.0;
+    for (int j = 0; j < n; ++j)
+      if (j != i) prod *= (xi[i] - xi[j]);
+    bw[i] = 1.0 / prod;
+  }
+  for (int t = 0; t <= 2 * p; ++t) {
+    const int sidx = t >= p ? 1 : 0;
+    const double xc = 0.5 * (sidx + xi[t - sidx * p]);
+    int hit = -1;
+    for (int k = 0; k < n; ++k)
+      if (xc == xi[k]) hit = k;
+    double denom = 0.0;
+    if (hit < 0)
+      for (int j = 0; j < n; ++j) denom += bw[j] / (xc - xi[j]);
+    for (int i = 0; i < n; ++i)
+      M[t * n + i] = hit >= 0 ? (i == hit ? 1.0 : 0.0) : (bw[i] / (xc - xi[i])) / denom;
+  }
+  return ELAS_OK;
+}
+
 }  // namespace elas

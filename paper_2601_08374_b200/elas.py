@@ -27,7 +27,8 @@ EXPORTED = ["elas_create", "elas_apply", "elas_apply_host", "elas_interface_add"
             "elas_last_error", "elas_slab_range", "elas_tables", "elas_nccl_unique_id", "elas_version",
             "elas_profile", "elas_profile_read", "elas_create_ex", "elas_variant",
             "elas_diagonal", "elas_cheb_create", "elas_cheb_lambda_max", "elas_cheb_apply",
-            "elas_cheb_destroy", "elas_pcg"]
+            "elas_cheb_destroy", "elas_pcg", "elas_gmg_create", "elas_gmg_level_op", "elas_gmg_levels",
+            "elas_gmg_set_stream", "elas_gmg_apply", "elas_pcg_gmg", "elas_gmg_destroy", "elas_gmg_transfer"]
 PC_NONE, PC_JACOBI, PC_CHEBYSHEV = 0, 1, 2
 
 
@@ -112,6 +113,24 @@ def load(path=None):
     lib.elas_pcg.restype = ctypes.c_int
     lib.elas_pcg.argtypes = [P, ctypes.c_int, P, P, P, ctypes.c_double, ctypes.c_int,
                              ctypes.POINTER(elas_solve_report), D]
+    lib.elas_gmg_create.restype = P
+    lib.elas_gmg_create.argtypes = [ctypes.POINTER(elas_mesh), ctypes.c_int, ctypes.c_int, D, D, ctypes.c_int,
+                                    ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_ulonglong,
+                                    ctypes.c_double, ctypes.c_int, ctypes.c_int]
+    lib.elas_gmg_level_op.restype = P
+    lib.elas_gmg_level_op.argtypes = [P, ctypes.c_int]
+    lib.elas_gmg_levels.restype = ctypes.c_int
+    lib.elas_gmg_levels.argtypes = [P]
+    lib.elas_gmg_set_stream.restype = ctypes.c_int
+    lib.elas_gmg_set_stream.argtypes = [P, P]
+    lib.elas_gmg_apply.restype = ctypes.c_int
+    lib.elas_gmg_apply.argtypes = [P, P, P]
+    lib.elas_pcg_gmg.restype = ctypes.c_int
+    lib.elas_pcg_gmg.argtypes = [P, P, P, P, ctypes.c_double, ctypes.c_int, ctypes.POINTER(elas_solve_report), D]
+    lib.elas_gmg_transfer.restype = ctypes.c_int
+    lib.elas_gmg_transfer.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P]
+    lib.elas_gmg_destroy.restype = None
+    lib.elas_gmg_destroy.argtypes = [P]
     _lib = lib
     return lib
 
@@ -177,10 +196,8 @@ def elas_variant(h):
     return load().elas_variant(h)
 
 
-def elas_create_ex(nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0), faces=0,
-                   rank=0, nranks=1, nccl_id=None, variant=VARIANT_AUTO):
-    """elas_create with an explicit kernel variant (VARIANT_AUTO / _SIMT / _TENSOR / _THREAD / _FOLDED)."""
-    lib = load()
+def _mesh_args(nx, ny, nz, lam, mu, vertices, lengths, faces, rank, nranks, nccl_id):
+    """Marshal an elas_mesh; returns (mesh, lam array, mu array, keep-alive list)."""
     lam_a = np.ascontiguousarray(np.asarray(lam, dtype=np.float64).reshape(-1))
     mu_a = np.ascontiguousarray(np.asarray(mu, dtype=np.float64).reshape(-1))
     per_elem = int(lam_a.size > 1 or mu_a.size > 1)
@@ -206,6 +223,14 @@ def elas_create_ex(nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 
         idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
         m.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
     m.rank, m.nranks = rank, nranks
+    return m, lam_a, mu_a, [V, idbuf]
+
+
+def elas_create_ex(nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0), faces=0,
+                   rank=0, nranks=1, nccl_id=None, variant=VARIANT_AUTO):
+    """elas_create with an explicit kernel variant (VARIANT_AUTO / _SIMT / _TENSOR / _THREAD / _FOLDED)."""
+    lib = load()
+    m, lam_a, mu_a, keep = _mesh_args(nx, ny, nz, lam, mu, vertices, lengths, faces, rank, nranks, nccl_id)
     h = lib.elas_create_ex(ctypes.byref(m), p, q, _dptr(lam_a), _dptr(mu_a), int(variant))
     if not h:
         raise ElasError(ELAS_EINVAL, f"elas_create: {elas_last_error()}")
@@ -379,6 +404,68 @@ class Chebyshev:
     def close(self):
         if self.h:
             elas_cheb_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class GMG:
+    """Owns one elas_gmg handle: the V-cycle hierarchy built from a fine mesh (C ABI
+    elas_gmg_create).  `op` is a non-owning view of the finest level's operator."""
+
+    def __init__(self, nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0), faces=0, levels=2,
+                 order=3, alpha=0.1, beta=1.1, power_iters=10, seed=1, coarse_rtol=-1.0, coarse_maxit=20,
+                 variant=VARIANT_AUTO, stream=None):
+        lib = load()
+        m, lam_a, mu_a, keep = _mesh_args(nx, ny, nz, lam, mu, vertices, lengths, faces, 0, 1, None)
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream()
+        self.h = lib.elas_gmg_create(ctypes.byref(m), p, q, _dptr(lam_a), _dptr(mu_a), levels, order, alpha, beta,
+                                     power_iters, seed, coarse_rtol, coarse_maxit, int(variant))
+        if not self.h:
+            raise ElasError(ELAS_EINVAL, f"elas_gmg_create: {elas_last_error()}")
+        _check(lib.elas_gmg_set_stream(self.h, stream.cuda_stream if hasattr(stream, "cuda_stream") else stream),
+               "elas_gmg_set_stream")
+        self.levels = lib.elas_gmg_levels(self.h)
+        self.op_h = lib.elas_gmg_level_op(self.h, 0)
+        self.local_dofs = load().elas_local_dofs(self.op_h)
+
+    @classmethod
+    def from_problem(cls, P, **kw):
+        return cls(P.nx, P.ny, P.nz, P.p, P.q, P.lam, P.mu, P.vertices, (P.lx, P.ly, P.lz), P.dirichlet_faces, **kw)
+
+    def level_op(self, level):
+        return load().elas_gmg_level_op(self.h, level)
+
+    def apply(self, b, x):
+        """One V-cycle: x = M b."""
+        _check(load().elas_gmg_apply(self.h, _ptr(b), _ptr(x)), "elas_gmg_apply")
+
+    def transfer(self, level, restrict, src, dst):
+        _check(load().elas_gmg_transfer(self.h, level, int(restrict), _ptr(src), _ptr(dst)), "elas_gmg_transfer")
+
+    def level_dofs(self, level):
+        return load().elas_local_dofs(self.level_op(level))
+
+    def apply_op(self, x, y):
+        """The finest-level operator: y = A x."""
+        _check(load().elas_apply(self.op_h, _ptr(x), _ptr(y)), "elas_apply")
+
+    def pcg(self, b, x, rtol=1e-8, maxit=500, history=False):
+        rep = elas_solve_report()
+        hist = np.zeros(maxit + 1) if history else None
+        _check(load().elas_pcg_gmg(self.op_h, self.h, _ptr(b), _ptr(x), rtol, maxit, ctypes.byref(rep),
+                                   _dptr(hist) if history else None), "elas_pcg_gmg")
+        return rep.iterations, bool(rep.converged), rep.rel_residual, (hist[:rep.iterations + 1] if history else None)
+
+    def close(self):
+        if self.h:
+            load().elas_gmg_destroy(self.h)
             self.h = None
 
     def __del__(self):
