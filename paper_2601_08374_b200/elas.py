@@ -321,6 +321,50 @@ def elas_pcg(h, precond, cheb, b, x, rtol, maxit, history=False):
     return rep.iterations, bool(rep.converged), rep.rel_residual, (hist[:rep.iterations + 1] if history else None)
 
 
+def elas_gmg_create(nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0), faces=0, levels=2,
+                    order=3, alpha=0.1, beta=1.1, power_iters=10, seed=1, coarse_rtol=-1.0, coarse_maxit=20,
+                    variant=VARIANT_AUTO):
+    m, lam_a, mu_a, keep = _mesh_args(nx, ny, nz, lam, mu, vertices, lengths, faces, 0, 1, None)
+    g = load().elas_gmg_create(ctypes.byref(m), p, q, _dptr(lam_a), _dptr(mu_a), levels, order, alpha, beta,
+                               power_iters, seed, coarse_rtol, coarse_maxit, int(variant))
+    if not g:
+        raise ElasError(ELAS_EINVAL, f"elas_gmg_create: {elas_last_error()}")
+    return g
+
+
+def elas_gmg_level_op(g, level):
+    return load().elas_gmg_level_op(g, level)
+
+
+def elas_gmg_levels(g):
+    return load().elas_gmg_levels(g)
+
+
+def elas_gmg_set_stream(g, stream):
+    s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+    _check(load().elas_gmg_set_stream(g, s), "elas_gmg_set_stream")
+
+
+def elas_gmg_apply(g, b, x):
+    _check(load().elas_gmg_apply(g, _ptr(b), _ptr(x)), "elas_gmg_apply")
+
+
+def elas_gmg_transfer(g, level, restrict, src, dst):
+    _check(load().elas_gmg_transfer(g, level, int(restrict), _ptr(src), _ptr(dst)), "elas_gmg_transfer")
+
+
+def elas_pcg_gmg(h, g, b, x, rtol, maxit, history=False):
+    rep = elas_solve_report()
+    hist = np.zeros(maxit + 1) if history else None
+    _check(load().elas_pcg_gmg(h, g, _ptr(b), _ptr(x), rtol, maxit, ctypes.byref(rep),
+                               _dptr(hist) if history else None), "elas_pcg_gmg")
+    return rep.iterations, bool(rep.converged), rep.rel_residual, (hist[:rep.iterations + 1] if history else None)
+
+
+def elas_gmg_destroy(g):
+    load().elas_gmg_destroy(g)
+
+
 # ------------------------------------------------------------------ convenience wrapper
 
 class Operator:
@@ -415,57 +459,48 @@ class Chebyshev:
 
 class GMG:
     """Owns one elas_gmg handle: the V-cycle hierarchy built from a fine mesh (C ABI
-    elas_gmg_create).  `op` is a non-owning view of the finest level's operator."""
+    elas_gmg_create).  `op_h` is a non-owning handle of the finest level's operator."""
 
     def __init__(self, nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0), faces=0, levels=2,
                  order=3, alpha=0.1, beta=1.1, power_iters=10, seed=1, coarse_rtol=-1.0, coarse_maxit=20,
                  variant=VARIANT_AUTO, stream=None):
-        lib = load()
-        m, lam_a, mu_a, keep = _mesh_args(nx, ny, nz, lam, mu, vertices, lengths, faces, 0, 1, None)
+        self.h = elas_gmg_create(nx, ny, nz, p, q, lam, mu, vertices, lengths, faces, levels, order, alpha, beta,
+                                 power_iters, seed, coarse_rtol, coarse_maxit, variant)
         if stream is None:
             import torch
             stream = torch.cuda.current_stream()
-        self.h = lib.elas_gmg_create(ctypes.byref(m), p, q, _dptr(lam_a), _dptr(mu_a), levels, order, alpha, beta,
-                                     power_iters, seed, coarse_rtol, coarse_maxit, int(variant))
-        if not self.h:
-            raise ElasError(ELAS_EINVAL, f"elas_gmg_create: {elas_last_error()}")
-        _check(lib.elas_gmg_set_stream(self.h, stream.cuda_stream if hasattr(stream, "cuda_stream") else stream),
-               "elas_gmg_set_stream")
-        self.levels = lib.elas_gmg_levels(self.h)
-        self.op_h = lib.elas_gmg_level_op(self.h, 0)
-        self.local_dofs = load().elas_local_dofs(self.op_h)
+        elas_gmg_set_stream(self.h, stream)
+        self.levels = elas_gmg_levels(self.h)
+        self.op_h = elas_gmg_level_op(self.h, 0)
+        self.local_dofs = elas_local_dofs(self.op_h)
 
     @classmethod
     def from_problem(cls, P, **kw):
         return cls(P.nx, P.ny, P.nz, P.p, P.q, P.lam, P.mu, P.vertices, (P.lx, P.ly, P.lz), P.dirichlet_faces, **kw)
 
     def level_op(self, level):
-        return load().elas_gmg_level_op(self.h, level)
+        return elas_gmg_level_op(self.h, level)
+
+    def level_dofs(self, level):
+        return elas_local_dofs(self.level_op(level))
 
     def apply(self, b, x):
         """One V-cycle: x = M b."""
-        _check(load().elas_gmg_apply(self.h, _ptr(b), _ptr(x)), "elas_gmg_apply")
+        elas_gmg_apply(self.h, b, x)
 
     def transfer(self, level, restrict, src, dst):
-        _check(load().elas_gmg_transfer(self.h, level, int(restrict), _ptr(src), _ptr(dst)), "elas_gmg_transfer")
-
-    def level_dofs(self, level):
-        return load().elas_local_dofs(self.level_op(level))
+        elas_gmg_transfer(self.h, level, restrict, src, dst)
 
     def apply_op(self, x, y):
         """The finest-level operator: y = A x."""
-        _check(load().elas_apply(self.op_h, _ptr(x), _ptr(y)), "elas_apply")
+        elas_apply(self.op_h, x, y)
 
     def pcg(self, b, x, rtol=1e-8, maxit=500, history=False):
-        rep = elas_solve_report()
-        hist = np.zeros(maxit + 1) if history else None
-        _check(load().elas_pcg_gmg(self.op_h, self.h, _ptr(b), _ptr(x), rtol, maxit, ctypes.byref(rep),
-                                   _dptr(hist) if history else None), "elas_pcg_gmg")
-        return rep.iterations, bool(rep.converged), rep.rel_residual, (hist[:rep.iterations + 1] if history else None)
+        return elas_pcg_gmg(self.op_h, self.h, b, x, rtol, maxit, history)
 
     def close(self):
         if self.h:
-            load().elas_gmg_destroy(self.h)
+            elas_gmg_destroy(self.h)
             self.h = None
 
     def __del__(self):
