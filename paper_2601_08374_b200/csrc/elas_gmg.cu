@@ -13,7 +13,8 @@
 // * V-cycle: x = S(b, 0); r = b - A x (constrained rows 0); b_c = R r (constrained 0);
 //   x_c = V(b_c); x += P x_c; x = S(b, x).  Coarsest: PCG preconditioned by the coarse
 //   Chebyshev smoother, either to a tolerance (synchronising) or a fixed iteration count (no
-//   host round trip; the default).
+//   host round trip; the default).  In the default mode the whole V-cycle (~40 launches per
+//   level, mostly on tiny coarse grids) is captured once into a CUDA graph and replayed.
 #include <cmath>
 #include <string>
 #include <vector>
@@ -29,6 +30,14 @@ struct elas_gmg {
   double* M1 = nullptr;                 // (2p+1) x (p+1) interpolation weights
   double coarse_rtol = -1.0;
   int coarse_maxit = 20;
+  // CUDA graph of one V-cycle (fixed-length coarse solve => no host synchronisation inside), for
+  // the (b, x) pointers it was captured with; replayed on a private stream ordered after/before
+  // the ops' stream by events (the legacy default stream cannot be captured)
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const double* gb = nullptr;
+  double* gx = nullptr;
 };
 
 namespace elas {
@@ -196,8 +205,43 @@ int vcycle(elas_gmg* g, int l, const double* b, double* x) {
   return cheb_run(g->chebs[l], b, x, false);                          // post-smoothing
 }
 
+int vcycle_graph(elas_gmg* g, const double* b, double* x) {
+  if (g->coarse_rtol > 0.0) return vcycle(g, 0, b, x);        // synchronising coarse solve: eager
+  cudaStream_t user = g->ops[0]->stream;
+  int rc;
+  if (!g->gexec || g->gb != b || g->gx != x) {
+    if (g->gexec) { cudaGraphExecDestroy(g->gexec); g->gexec = nullptr; }
+    if ((rc = vcycle(g, 0, b, x))) return rc;                 // eager run: first-launch setup outside capture
+    GK(cudaStreamSynchronize(user), "cudaStreamSynchronize");
+    for (auto* o : g->ops) o->stream = g->gstream;
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(g->gstream, cudaStreamCaptureModeThreadLocal);
+    rc = e ? gfail(e, "cudaStreamBeginCapture") : vcycle(g, 0, b, x);
+    cudaError_t e2 = cudaStreamEndCapture(g->gstream, &graph);
+    for (auto* o : g->ops) o->stream = user;
+    if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
+    GK(e2, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&g->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    GK(e, "cudaGraphInstantiate");
+    g->gb = b;
+    g->gx = x;
+    return ELAS_OK;                                             // the eager run produced x
+  }
+  GK(cudaEventRecord(g->ev_in, user), "cudaEventRecord");
+  GK(cudaStreamWaitEvent(g->gstream, g->ev_in, 0), "cudaStreamWaitEvent");
+  GK(cudaGraphLaunch(g->gexec, g->gstream), "cudaGraphLaunch");
+  GK(cudaEventRecord(g->ev_out, g->gstream), "cudaEventRecord");
+  GK(cudaStreamWaitEvent(user, g->ev_out, 0), "cudaStreamWaitEvent");
+  return ELAS_OK;
+}
+
 void free_gmg(elas_gmg* g) {
   if (!g) return;
+  if (g->gexec) cudaGraphExecDestroy(g->gexec);
+  if (g->gstream) cudaStreamDestroy(g->gstream);
+  if (g->ev_in) cudaEventDestroy(g->ev_in);
+  if (g->ev_out) cudaEventDestroy(g->ev_out);
   for (auto* c : g->chebs) elas_cheb_destroy(c);
   for (auto* o : g->ops) elas_destroy(o);
   for (auto* v : {&g->vb, &g->vx, &g->vr, &g->ta, &g->tb})
@@ -281,6 +325,13 @@ elas_gmg* elas_gmg_create(const elas_mesh* fine, int p, int q, const double* lam
     if (!ch) { elas::free_gmg(g); return nullptr; }
     g->chebs.push_back(ch);
   }
+  if (cudaStreamCreateWithFlags(&g->gstream, cudaStreamNonBlocking) ||
+      cudaEventCreateWithFlags(&g->ev_in, cudaEventDisableTiming) ||
+      cudaEventCreateWithFlags(&g->ev_out, cudaEventDisableTiming)) {
+    set_error("elas_gmg_create: stream/event creation failed");
+    elas::free_gmg(g);
+    return nullptr;
+  }
   std::vector<double> Mh((size_t)(2 * p + 1) * (p + 1));
   elas::host_prolongation_1d(p, Mh.data());
   cudaError_t e = cudaMalloc(&g->M1, sizeof(double) * Mh.size());
@@ -325,6 +376,7 @@ int elas_gmg_levels(const elas_gmg* g) { return g ? g->levels : -1; }
 int elas_gmg_set_stream(elas_gmg* g, void* stream) {
   if (!g) { elas::set_error("elas_gmg_set_stream: NULL"); return ELAS_EINVAL; }
   for (auto* o : g->ops) elas_set_stream(o, stream);
+  if (g->gexec) { cudaGraphExecDestroy(g->gexec); g->gexec = nullptr; }
   return ELAS_OK;
 }
 
@@ -339,7 +391,7 @@ int elas_gmg_transfer(elas_gmg* g, int level, int restrict_, const double* in, d
 int elas_gmg_apply(elas_gmg* g, const double* b, double* x) {
   if (!g || !b || !x) { elas::set_error("elas_gmg_apply: NULL argument"); return ELAS_EINVAL; }
   if (b == x) { elas::set_error("elas_gmg_apply: b and x must not alias"); return ELAS_EINVAL; }
-  return elas::vcycle(g, 0, b, x);
+  return elas::vcycle_graph(g, b, x);
 }
 
 int elas_pcg_gmg(elas_op* op, elas_gmg* g, const double* b, double* x, double rtol, int maxit,
@@ -350,7 +402,7 @@ int elas_pcg_gmg(elas_op* op, elas_gmg* g, const double* b, double* x, double rt
     return ELAS_EINVAL;
   }
   if (b == x || maxit < 0 || !(rtol >= 0.0)) { elas::set_error("elas_pcg_gmg: need b != x, maxit >= 0, rtol >= 0"); return ELAS_EINVAL; }
-  return elas::pcg_core(op, elas::PC_CALLBACK, [g](const double* r, double* z) { return elas::vcycle(g, 0, r, z); }, b,
+  return elas::pcg_core(op, elas::PC_CALLBACK, [g](const double* r, double* z) { return elas::vcycle_graph(g, r, z); }, b,
                         x, rtol, maxit, true, rep, history);
 }
 
