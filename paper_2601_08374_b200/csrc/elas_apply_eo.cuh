@@ -33,7 +33,9 @@ struct Fold {
 
 // CTA size and register target of the folded kernel per degree (ELAS_EO_NT_P<p>,
 // ELAS_EO_MINB_P<p> override; measured by tools/ab_libs.sh)
-template <int P> struct NtEO { static constexpr int value = ELAS_NT; };
+// measured (tools/ab_libs.sh, config 4): 256 threads at p = 5 (EB = 5: 245 of 256 stage-X lines
+// busy) 26.0 -> 28.5 GDoF/s; 160/192/224/256 lose at p = 3, 4, 6, 7, 8
+template <int P> struct NtEO { static constexpr int value = P == 5 ? 256 : ELAS_NT; };
 template <int P> struct MinbEO { static constexpr int value = P == 2 ? 4 : MinBlocks<P>::value; };
 #ifdef ELAS_EO_NT_P2
 template <> struct NtEO<2> { static constexpr int value = ELAS_EO_NT_P2; };
