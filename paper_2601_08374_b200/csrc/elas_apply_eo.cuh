@@ -97,6 +97,9 @@ using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEO<P>::value, (int)sizeof(T)>;
 // whole-CTA TMA staging of qdata where two CTAs fit (elas_apply.cuh); off at p = 2, which
 // runs faster at 4 CTAs/SM without it (12.5 -> 16 GDoF/s)
 template <int P> struct StageEO { static constexpr bool value = P != 2; };
+#ifndef ELAS_QD_L1PF
+#define ELAS_QD_L1PF 0
+#endif
 #ifndef ELAS_QD_RING_ALIAS
 #define ELAS_QD_RING_ALIAS 1
 #endif
@@ -443,6 +446,13 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, MinbEO<P>::value)
 #pragma unroll
           for (int f = 0; f < 9; ++f) An[f] = qp[((a1 + 1) * 9 + f) * Q * Q];
         }
+#if ELAS_QD_L1PF > 0
+        if (!RG::STAGE && a1 + 1 + ELAS_QD_L1PF < Q) {   // L1 prefetch further ahead (no registers)
+#pragma unroll
+          for (int f = 0; f < 9; ++f)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(qp + ((a1 + 1 + ELAS_QD_L1PF) * 9 + f) * Q * Q));
+        }
+#endif
       }
       T G[3][3];
 #pragma unroll
