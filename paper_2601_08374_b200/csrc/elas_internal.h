@@ -77,6 +77,7 @@ cudaError_t launch_qdata(int p, int q, int layout, const Slab& s, const double* 
                          const double* mu, const double* gpts, const double* gw, double* qd,
                          double* rr, int* bad, cudaStream_t st);
 cudaError_t launch_init(const Slab& s, const double* x, double* y, cudaStream_t st);
+cudaError_t launch_init_planes(const Slab& s, int K0, int K1, const double* x, double* y, cudaStream_t st);
 cudaError_t launch_plane_add(const Slab& s, int which_plane, double* y, const double* halo,
                              cudaStream_t st);
 

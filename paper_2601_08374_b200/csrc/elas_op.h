@@ -20,6 +20,8 @@ struct elas_op {
   float* tabf = nullptr;            // FP32 copy of tab (mixed-precision folded kernel)
   double* xs = nullptr;             // staging for elas_apply_host
   double* ys = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;   // copy streams of the chunked host apply
+  std::vector<cudaEvent_t> host_ev;            // per chunk: x landed, chunk computed
   cudaStream_t stream = nullptr;
   // multi-GPU
   ncclComm_t comm = nullptr;

@@ -111,6 +111,24 @@ __global__ void init_kernel(Slab s, const double* __restrict__ x, double* __rest
   }
 }
 
+// init on node planes [K0, K1) only (the chunked host apply)
+__global__ void init_planes_kernel(Slab s, int K0, int K1, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t plane = (int64_t)s.Nx * s.Ny;
+  const int64_t per_c = (int64_t)(K1 - K0) * plane;
+  const bool bc = s.faces != 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 3 * per_c; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / per_c;
+    const int64_t node = (int64_t)K0 * plane + (t - c * per_c);
+    const int64_t idx = c * s.nodes + node;
+    double v = 0.0;
+    if (bc) {
+      const int I = (int)(node % s.Nx), J = (int)((node / s.Nx) % s.Ny), K = (int)(node / plane);
+      if (constrained_node(I, J, K, s)) v = x[idx];
+    }
+    y[idx] = v;
+  }
+}
+
 __global__ void plane_add_kernel(Slab s, int K, double* __restrict__ y, const double* __restrict__ halo) {
   const int64_t plane = (int64_t)s.Nx * s.Ny;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 3 * plane; t += (int64_t)gridDim.x * blockDim.x) {
@@ -147,6 +165,13 @@ cudaError_t launch_qdata(int p, int q, int layout, const Slab& s, const double* 
 
 cudaError_t launch_init(const Slab& s, const double* x, double* y, cudaStream_t st) {
   init_kernel<<<grid_for(3 * s.nodes, 256), 256, 0, st>>>(s, x, y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_planes(const Slab& s, int K0, int K1, const double* x, double* y, cudaStream_t st) {
+  if (K1 <= K0) return cudaSuccess;
+  const int64_t n = 3 * (int64_t)(K1 - K0) * s.Nx * s.Ny;
+  init_planes_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, K0, K1, x, y);
   return cudaGetLastError();
 }
 

@@ -423,3 +423,20 @@ def test_folded_f32_config4_sampled():
     op.close()
     rows = sample_rows(P, 128, 6)
     assert rel_l2(y[rows], oracle.apply_rows(oracle_mesh(P), P.x, rows)) <= TOL_F32
+
+
+@pytest.mark.parametrize("p,dims,faces", [(2, (3, 2, 7), 16 | 32 | 1), (6, (2, 2, 19), 0), (1, (5, 4, 33), 63)])
+def test_apply_host_chunked_pipeline(p, dims, faces):
+    """elas_apply_host pipelines H2D / apply / D2H over z-chunks of element layers: equal to the
+    device apply (chunk-boundary planes, Dirichlet z faces, uneven chunk sizes, nz > 16 chunks)."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_problem("t", *dims, p, p + 2, perturb=True, lognormal_material=True, faces=faces, seed=77 + p)
+    op = Operator.from_problem(P)
+    xh = torch.from_numpy(P.x).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    op.apply_host(xh, yh)
+    yd = gpu_apply(P, op=op)
+    op.close()
+    assert rel_l2(yh.numpy(), yd) <= 1e-15
+    assert rel_l2(yh.numpy(), oracle.apply(oracle_mesh(P), P.x)) <= TOL
