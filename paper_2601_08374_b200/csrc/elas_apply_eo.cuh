@@ -36,7 +36,7 @@ struct Fold {
 // measured (tools/ab_libs.sh, config 4): 256 threads at p = 5 (EB = 5: 245 of 256 stage-X lines
 // busy) 26.0 -> 28.5 GDoF/s; 160/192/224/256 lose at p = 3, 4, 6, 7, 8
 template <int P> struct NtEO { static constexpr int value = P == 5 ? 256 : ELAS_NT; };
-template <int P> struct MinbEO { static constexpr int value = P == 2 ? 4 : MinBlocks<P>::value; };
+template <int P> struct MinbEO { static constexpr int value = P == 2 ? 4 : P == 3 ? 3 : MinBlocks<P>::value; };
 #ifdef ELAS_EO_NT_P2
 template <> struct NtEO<2> { static constexpr int value = ELAS_EO_NT_P2; };
 #endif
@@ -96,7 +96,10 @@ using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEO<P>::value, (int)sizeof(T)>;
 #endif
 // whole-CTA TMA staging of qdata where two CTAs fit (elas_apply.cuh); off at p = 2, which
 // runs faster at 4 CTAs/SM without it (12.5 -> 16 GDoF/s)
-template <int P> struct StageEO { static constexpr bool value = P != 2; };
+#ifndef ELAS_EO_NOSTAGE_P3
+#define ELAS_EO_NOSTAGE_P3 1   // measured: p = 3 without staging at 3 CTAs/SM 21.4 -> 22.2
+#endif
+template <int P> struct StageEO { static constexpr bool value = P != 2 && !(P == 3 && ELAS_EO_NOSTAGE_P3); };
 #ifndef ELAS_QD_L1PF
 #define ELAS_QD_L1PF 0
 #endif
