@@ -80,6 +80,11 @@ template <> struct MinbEO<7> { static constexpr int value = ELAS_EO_MINB_P7; };
 template <> struct MinbEO<8> { static constexpr int value = ELAS_EO_MINB_P8; };
 #endif
 
+// register target of the FP32 (mixed-precision) instances: half-size registers leave room for more
+// CTAs per SM where one element per CTA would otherwise cap the warps (p >= 7)
+// (measured, config 4: p7 23.9 -> 41.3 GDoF/s at 4 CTAs/SM, p8 31.6 -> 40.9 at 3)
+template <int P> struct MinbEO32 { static constexpr int value = P == 7 ? 4 : P == 8 ? 3 : MinbEO<P>::value; };
+
 template <int P, int Q, typename T = double>
 using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEO<P>::value, (int)sizeof(T)>;
 
@@ -168,7 +173,7 @@ __device__ __forceinline__ void fold_in(const T (&u)[3][N], T (&up)[3][NE], T (&
 }
 
 template <int P, int Q, typename T>
-__global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, MinbEO<P>::value)
+__global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<P>::value : MinbEO<P>::value)
     apply_eo_kernel(const double* __restrict__ x, double* __restrict__ y, const T* __restrict__ qd,
                     const double* __restrict__ rr, const T* __restrict__ tables, Slab s,
                     int64_t e_begin, int64_t e_end, int pref_ctas) {
