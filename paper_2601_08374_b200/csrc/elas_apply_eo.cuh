@@ -82,8 +82,14 @@ template <> struct MinbEO<8> { static constexpr int value = ELAS_EO_MINB_P8; };
 
 // register target of the FP32 (mixed-precision) instances: half-size registers leave room for more
 // CTAs per SM where one element per CTA would otherwise cap the warps (p >= 7)
-// (measured, config 4: p7 23.9 -> 41.3 GDoF/s at 4 CTAs/SM, p8 31.6 -> 40.9 at 3)
-template <int P> struct MinbEO32 { static constexpr int value = P == 7 ? 4 : P == 8 ? 3 : MinbEO<P>::value; };
+// (measured, config 4: p7 23.9 -> 41.3 GDoF/s at 4 CTAs/SM, p8 31.6 -> 40.9 at 3, p5 (256 threads)
+// 35.8 -> 46.4 at 2)
+#ifndef ELAS_EO32_MINB_LO
+#define ELAS_EO32_MINB_LO 0
+#endif
+template <int P> struct MinbEO32 {
+  static constexpr int value = P == 7 ? 4 : P == 8 ? 3 : P == 5 ? 2 : (ELAS_EO32_MINB_LO > 0 ? ELAS_EO32_MINB_LO : MinbEO<P>::value);
+};
 
 template <int P, int Q, typename T = double>
 using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEO<P>::value, (int)sizeof(T)>;
