@@ -109,6 +109,12 @@ elas_op* elas_create(const elas_mesh* mesh, int p, int q, const double* lambda, 
 elas_op* elas_create_ex(const elas_mesh* mesh, int p, int q, const double* lambda, const double* mu,
                         int variant);
 
+/* Bitwise-reproducible applies: on != 0 splits the apply into
+ * 8 launches, one per element color (parity per axis) in a fixed order; no two elements of a
+ * color share a node, so every node gets one contribution per launch and the sum order is fixed.  Folded
+ * variants only (ELAS_EINVAL otherwise).  Same result to rounding; y identical run to run. */
+int elas_set_deterministic(elas_op* op, int on);
+
 /* The resolved variant of an op (ELAS_VARIANT_SIMT, _TENSOR, _THREAD, _FOLDED or _FOLDED_F32), -1 if NULL. */
 int elas_variant(const elas_op* op);
 

@@ -47,7 +47,7 @@ DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
   cudaError_t apply_eo_info_p##P(int q, int fp32, ApplyLaunch* info);                            \
   cudaError_t apply_eo_launch_p##P(int q, int fp32, const Slab& s, const double* x, double* y,   \
                                    const void* qd, const double* rr, const void* tables,        \
-                                   int64_t e_begin, int64_t e_end, cudaStream_t st);
+                                   int64_t e_begin, int64_t e_end, cudaStream_t st, const int* color);
 DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
 #undef DECL
 
@@ -89,9 +89,9 @@ cudaError_t apply_eo_info(int p, int q, int fp32, ApplyLaunch* info) {
 
 cudaError_t apply_eo_launch(int p, int q, int fp32, const Slab& s, const double* x, double* y, const void* qd,
                             const double* rr, const void* tables, int64_t e_begin, int64_t e_end,
-                            cudaStream_t st) {
+                            cudaStream_t st, const int* color) {
   switch (p) {
-#define CASE(P) case P: return apply_eo_launch_p##P(q, fp32, s, x, y, qd, rr, tables, e_begin, e_end, st);
+#define CASE(P) case P: return apply_eo_launch_p##P(q, fp32, s, x, y, qd, rr, tables, e_begin, e_end, st, color);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
     default: return cudaErrorInvalidValue;
@@ -281,7 +281,28 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
     op->prof_used += 2;
     CUDA_OR(cudaEventRecord(ev0, st), "cudaEventRecord");
   }
-  cudaError_t e = op->variant == ELAS_VARIANT_TENSOR
+  cudaError_t e;
+  if (op->deterministic) {
+    // 8 colors in a fixed order over the element layers [e0, e1) (whole layers: e0, e1 are
+    // multiples of nx ny); a color's lattice: parity (cx, cy, cz) per axis
+    const Slab& s = op->slab;
+    const int64_t layer = (int64_t)s.nx * s.ny;
+    const int z0 = (int)(e0 / layer), z1 = (int)(e1 / layer);
+    e = cudaSuccess;
+    for (int c = 0; c < 8 && e == cudaSuccess; ++c) {
+      const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
+      const int ncx = (s.nx - cx + 1) / 2, ncy = (s.ny - cy + 1) / 2;
+      const int iz0 = (z0 - cz + 1) / 2 > 0 ? (z0 - cz + 1) / 2 : 0;   // first iz with 2 iz + cz >= z0
+      const int iz1 = (z1 - cz + 1) / 2 > 0 ? (z1 - cz + 1) / 2 : 0;   // first iz with 2 iz + cz >= z1
+      const int64_t cnt = (int64_t)ncx * ncy * (iz1 > iz0 ? iz1 - iz0 : 0);
+      if (cnt <= 0) continue;
+      const int cm[6] = {cx, cy, cz, ncx, ncy, iz0};
+      e = elas::apply_eo_launch(op->p, op->q, op->variant == ELAS_VARIANT_FOLDED_F32, s, x, y, op->qd, op->rr,
+                                op->variant == ELAS_VARIANT_FOLDED_F32 ? (const void*)op->tabf : (const void*)op->tab,
+                                0, cnt, st, cm);
+    }
+  } else
+  e = op->variant == ELAS_VARIANT_TENSOR
                       ? elas::apply_tc_launch(op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
                   : op->variant == ELAS_VARIANT_THREAD
                       ? elas::apply_p1t_launch(op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
@@ -484,6 +505,16 @@ int elas_profile_read(elas_op* op, double* ms, int64_t* launches) {
 }
 
 int elas_variant(const elas_op* op) { return op ? op->variant : -1; }
+
+int elas_set_deterministic(elas_op* op, int on) {
+  if (!op) { set_error("elas_set_deterministic: NULL op"); return ELAS_EINVAL; }
+  if (on && op->variant != ELAS_VARIANT_FOLDED && op->variant != ELAS_VARIANT_FOLDED_F32) {
+    set_error("elas_set_deterministic: the colored scatter exists for the folded variants only");
+    return ELAS_EINVAL;
+  }
+  op->deterministic = on != 0;
+  return ELAS_OK;
+}
 
 int elas_launches_per_apply(const elas_op* op) {
   if (!op) return -1;

@@ -164,6 +164,36 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Deterministic (colored) mode: the elements of one launch all have the same parity (cx, cy, cz)
+// per axis, so no two of them share a node: each node receives ONE contribution per launch and
+// the (fire-and-forget) atomic add y + v is order-free; the 8 colors run in a fixed order =>
+// bitwise reproducible y.  A plain read-modify-write would
+// be equally deterministic but exposes the load latency (measured 2x slower).  Linear index l in the launch -> (ix, iy, iz) of the color's lattice ->
+// element (2 ix + cx, 2 iy + cy, 2 (iz + iz0) + cz).  on = 0: l is the element id itself.
+struct ColorMap {
+  int on, cx, cy, cz, ncx, ncy, iz0;
+};
+
+template <bool COLORED>
+__device__ __forceinline__ int64_t elem_coords(const ColorMap& cm, const Slab& s, int64_t l, int& ex, int& ey,
+                                               int& ez) {
+  const uint32_t l32 = (uint32_t)l;
+  if constexpr (!COLORED) {
+    const uint32_t nx = (uint32_t)s.nx, ny = (uint32_t)s.ny;
+    const uint32_t exy = l32 / nx;
+    ex = (int)(l32 - exy * nx);
+    ez = (int)(exy / ny);
+    ey = (int)(exy - (uint32_t)ez * ny);
+    return l;
+  }
+  const uint32_t ncx = (uint32_t)cm.ncx, ncy = (uint32_t)cm.ncy;
+  const uint32_t ixy = l32 / ncx, ix = l32 - ixy * ncx, iz = ixy / ncy, iy = ixy - iz * ncy;
+  ex = 2 * (int)ix + cm.cx;
+  ey = 2 * (int)iy + cm.cy;
+  ez = 2 * ((int)iz + cm.iz0) + cm.cz;
+  return ex + (int64_t)s.nx * (ey + (int64_t)s.ny * ez);
+}
+
 // u (n values per component) -> even (ne) / odd (nh) halves
 template <int N, int NE, int NHX, typename T>
 __device__ __forceinline__ void fold_in(const T (&u)[3][N], T (&up)[3][NE], T (&um)[3][NHX]) {
@@ -178,11 +208,11 @@ __device__ __forceinline__ void fold_in(const T (&u)[3][N], T (&up)[3][NE], T (&
   }
 }
 
-template <int P, int Q, typename T>
+template <int P, int Q, typename T, bool COLORED>
 __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<P>::value : MinbEO<P>::value)
     apply_eo_kernel(const double* __restrict__ x, double* __restrict__ y, const T* __restrict__ qd,
                     const double* __restrict__ rr, const T* __restrict__ tables, Slab s,
-                    int64_t e_begin, int64_t e_end, int pref_ctas) {
+                    int64_t e_begin, int64_t e_end, int pref_ctas, ColorMap cm) {
   using C = CfgEO<P, Q, T>;
   using F = Fold<P, Q>;
   constexpr int N = C::N, NT = C::NT, EB = C::EB;
@@ -208,16 +238,29 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(sQ)),
-          "l"(qd + e0 * (int64_t)C::QDE), "r"(bytes), "r"(bar)
-          : "memory");
+      if constexpr (!COLORED) {
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(sQ)),
+            "l"(qd + e0 * (int64_t)C::QDE), "r"(bytes), "r"(bar)
+            : "memory");
+      } else {   // colored mode: the batch's elements are not contiguous, one bulk copy each
+        for (int el = 0; el < ne; ++el) {
+          int ex, ey, ez;
+          const int64_t e = elem_coords<COLORED>(cm, s, e0 + el, ex, ey, ez);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(sQ + el * C::QDE)),
+              "l"(qd + e * (int64_t)C::QDE), "r"((uint32_t)(sizeof(T) * C::QDE)), "r"(bar)
+              : "memory");
+        }
+      }
     }
   }
   // this thread's stage-X line (at most one: EB q^2 <= NT) and its qdata ring
   T* ring = smem + RG::OFF + tid;
   const bool has_line = tid < ne * Q * Q;
-  const T* qline = qd + (e0 + tid / (Q * Q)) * (int64_t)C::QDE + tid % (Q * Q);
+  int qex, qey, qez;
+  const T* qline = qd + elem_coords<COLORED>(cm, s, e0 + tid / (Q * Q), qex, qey, qez) * (int64_t)C::QDE + tid % (Q * Q);
   auto ring_issue = [&](int a1) {
     if (has_line) {
 #pragma unroll
@@ -239,13 +282,13 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   const int zi = tid % N, zj = (tid / N) % N, zel = tid / (N * N);
   T u[3][N];
   if (zcol) {
-    const uint32_t e32 = (uint32_t)(e0 + zel), nx = (uint32_t)s.nx, ny = (uint32_t)s.ny;
-    const uint32_t exy = e32 / nx, ex = e32 - exy * nx, ez = exy / ny, ey = exy - ez * ny;
-    const int I = (int)ex * P + zi, J = (int)ey * P + zj;
+    int ex, ey, ez;
+    elem_coords<COLORED>(cm, s, e0 + zel, ex, ey, ez);
+    const int I = ex * P + zi, J = ey * P + zj;
     const int64_t base = I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      const bool cons = bc && is_constrained(I, J, (int)ez * P + k, s);
+      const bool cons = bc && is_constrained(I, J, ez * P + k, s);
 #pragma unroll
       for (int c = 0; c < 3; ++c) u[c][k] = cons ? T(0) : (T)__ldg(x + c * s.nodes + base + k * plane);
     }
@@ -257,7 +300,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
 #if ELAS_L2_PREFETCH
   if (tid == 0 && pref_ctas > 0) {
     const int64_t pe0 = e0 + (int64_t)pref_ctas * EB;
-    if (pe0 < e_end) {
+    if (pe0 < e_end && !COLORED) {
       const int64_t pne = (e_end - pe0) < EB ? (e_end - pe0) : EB;
       const uintptr_t a0 = (uintptr_t)(qd + pe0 * (int64_t)C::QDE);
       const uintptr_t a1 = a0 + (uintptr_t)(pne * C::QDE * sizeof(T));
@@ -394,7 +437,8 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   for (int w = tid; w < ne * Q * Q; w += NT) {
     const int L = w % (Q * Q), el = w / (Q * Q);
     const int a3 = L % Q, a2 = L / Q;
-    const int64_t e = e0 + el;
+    int xex, xey, xez;
+    const int64_t e = elem_coords<COLORED>(cm, s, e0 + el, xex, xey, xez);
     T* line = sY + el * C::YE + a2 * C::S2 + a3 * N;
     T g[3][3][Q];
 #pragma unroll
@@ -597,9 +641,8 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   // ---------------- Stage Zt: folded transposed contraction in z + scatter-add ----------
   for (int w = tid; w < ne * N * N; w += NT) {
     const int i = w % N, j = (w / N) % N, el = w / (N * N);
-    const uint32_t e32 = (uint32_t)(e0 + el), nxu = (uint32_t)s.nx, nyu = (uint32_t)s.ny;
-    const uint32_t exy = e32 / nxu;
-    const int ex = (int)(e32 - exy * nxu), ez = (int)(exy / nyu), ey = (int)(exy - (uint32_t)ez * nyu);
+    int ex, ey, ez;
+    elem_coords<COLORED>(cm, s, e0 + el, ex, ey, ez);
     const T* src = sZ + el * C::ZE + j * N + i;
     T X[3][NE], Y[3][NE];
 #pragma unroll
@@ -650,41 +693,57 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
       const bool kmid = (N & 1) && k == NH;
       if (!(bc && is_constrained(I, J, ez * P + k, s))) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) atomicAdd(y + c * s.nodes + base + k * plane, (double)(kmid ? X[c][k] : X[c][k] + Y[c][k]));
+        for (int c = 0; c < 3; ++c) {
+          double* dst = y + c * s.nodes + base + k * plane;
+          const double v = (double)(kmid ? X[c][k] : X[c][k] + Y[c][k]);
+          atomicAdd(dst, v);   // colored mode: one contribution per node per launch => order-free
+        }
       }
       if (!kmid && !(bc && is_constrained(I, J, ez * P + N - 1 - k, s))) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) atomicAdd(y + c * s.nodes + base + (N - 1 - k) * plane, (double)(X[c][k] - Y[c][k]));
+        for (int c = 0; c < 3; ++c) {
+          double* dst = y + c * s.nodes + base + (N - 1 - k) * plane;
+          const double v = (double)(X[c][k] - Y[c][k]);
+          atomicAdd(dst, v);
+        }
       }
     }
   }
 }
 
-template <int P, int Q, typename T>
-cudaError_t launch_apply_eo_pq(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
-                               const void* tables, int64_t e_begin, int64_t e_end, cudaStream_t st) {
+template <int P, int Q, typename T, bool COLORED>
+cudaError_t launch_apply_eo_pqc(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
+                                const void* tables, int64_t e_begin, int64_t e_end, cudaStream_t st,
+                                const ColorMap& cm) {
   using C = CfgEO<P, Q, T>;
   using RG = RingEO<P, Q, T>;
   static bool attr_done = false;
   static int pref = -1;
   if (!attr_done) {
-    cudaError_t err = cudaFuncSetAttribute(apply_eo_kernel<P, Q, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)RG::smem);
+    cudaError_t err = cudaFuncSetAttribute(apply_eo_kernel<P, Q, T, COLORED>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::smem);
     if (err != cudaSuccess) return err;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_eo_kernel<P, Q, T>, C::NT, RG::smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_eo_kernel<P, Q, T, COLORED>, C::NT, RG::smem);
     pref = sms * (per_sm > 0 ? per_sm : 1);
     attr_done = true;
   }
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
   const int64_t grid = (ne + C::EB - 1) / C::EB;
-  apply_eo_kernel<P, Q, T><<<(unsigned)grid, C::NT, RG::smem, st>>>(x, y, static_cast<const T*>(qd), rr,
-                                                                     static_cast<const T*>(tables), s, e_begin,
-                                                                     e_end, pref);
+  apply_eo_kernel<P, Q, T, COLORED><<<(unsigned)grid, C::NT, RG::smem, st>>>(
+      x, y, static_cast<const T*>(qd), rr, static_cast<const T*>(tables), s, e_begin, e_end, pref, cm);
   return cudaGetLastError();
+}
+
+template <int P, int Q, typename T>
+cudaError_t launch_apply_eo_pq(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
+                               const void* tables, int64_t e_begin, int64_t e_end, cudaStream_t st,
+                               const ColorMap& cm) {
+  return cm.on ? launch_apply_eo_pqc<P, Q, T, true>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm)
+               : launch_apply_eo_pqc<P, Q, T, false>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm);
 }
 
 template <int P, int Q, typename T>
@@ -707,13 +766,16 @@ void info_eo_pq(ApplyLaunch* info) {
   }                                                                                             \
   cudaError_t apply_eo_launch_p##P(int q, int fp32, const Slab& s, const double* x, double* y,  \
                                    const void* qd, const double* rr, const void* tables,        \
-                                   int64_t e_begin, int64_t e_end, cudaStream_t st) {           \
+                                   int64_t e_begin, int64_t e_end, cudaStream_t st,             \
+                                   const int* color) {                                          \
+    ColorMap cm{0, 0, 0, 0, 0, 0, 0};                                                           \
+    if (color) cm = ColorMap{1, color[0], color[1], color[2], color[3], color[4], color[5]};    \
     if (q == P + 1)                                                                             \
-      return fp32 ? launch_apply_eo_pq<P, P + 1, float>(s, x, y, qd, rr, tables, e_begin, e_end, st) \
-                  : launch_apply_eo_pq<P, P + 1, double>(s, x, y, qd, rr, tables, e_begin, e_end, st); \
+      return fp32 ? launch_apply_eo_pq<P, P + 1, float>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm) \
+                  : launch_apply_eo_pq<P, P + 1, double>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm); \
     if (q == P + 2)                                                                             \
-      return fp32 ? launch_apply_eo_pq<P, P + 2, float>(s, x, y, qd, rr, tables, e_begin, e_end, st) \
-                  : launch_apply_eo_pq<P, P + 2, double>(s, x, y, qd, rr, tables, e_begin, e_end, st); \
+      return fp32 ? launch_apply_eo_pq<P, P + 2, float>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm) \
+                  : launch_apply_eo_pq<P, P + 2, double>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm); \
     return cudaErrorInvalidValue;                                                               \
   }                                                                                             \
   }

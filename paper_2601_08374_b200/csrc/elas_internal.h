@@ -35,9 +35,11 @@ int host_prolongation_1d(int p, double* M);
 // folded-SIMT variant (elas_apply_eo_p<P>.cu); fp32 != 0: the mixed-precision instance (FP32
 // qdata, tables and arithmetic; FP64 x, y and scatter)
 cudaError_t apply_eo_info(int p, int q, int fp32, ApplyLaunch* info);
+// color == nullptr: elements [e_begin, e_end) with atomic scatter.  color = {cx, cy, cz, ncx, ncy,
+// iz0}: the linear range [e_begin, e_end) of one color's element lattice, plain-RMW scatter.
 cudaError_t apply_eo_launch(int p, int q, int fp32, const Slab& s, const double* x, double* y, const void* qd,
                             const double* rr, const void* tables, int64_t e_begin, int64_t e_end,
-                            cudaStream_t st);
+                            cudaStream_t st, const int* color = nullptr);
 
 // Per-degree translation units (elas_apply_p<P>.cu) export these; q must be p+1 or p+2.
 // Returns cudaSuccess or an error; `info` only queries the configuration.

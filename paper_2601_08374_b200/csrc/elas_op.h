@@ -10,6 +10,7 @@
 struct elas_op {
   int p = 0, q = 0, rank = 0, nranks = 1;
   int variant = ELAS_VARIANT_SIMT;  // resolved kernel variant
+  bool deterministic = false;       // colored scatter (elas_set_deterministic)
   int32_t ez0 = 0, ez1 = 0;
   elas::Slab slab{};
   int device = 0;

@@ -28,7 +28,8 @@ EXPORTED = ["elas_create", "elas_apply", "elas_apply_host", "elas_interface_add"
             "elas_profile", "elas_profile_read", "elas_create_ex", "elas_variant",
             "elas_diagonal", "elas_cheb_create", "elas_cheb_lambda_max", "elas_cheb_apply",
             "elas_cheb_destroy", "elas_pcg", "elas_gmg_create", "elas_gmg_level_op", "elas_gmg_levels",
-            "elas_gmg_set_stream", "elas_gmg_apply", "elas_pcg_gmg", "elas_gmg_destroy", "elas_gmg_transfer"]
+            "elas_gmg_set_stream", "elas_gmg_apply", "elas_pcg_gmg", "elas_gmg_destroy", "elas_gmg_transfer",
+            "elas_set_deterministic"]
 PC_NONE, PC_JACOBI, PC_CHEBYSHEV = 0, 1, 2
 
 
@@ -127,6 +128,8 @@ def load(path=None):
     lib.elas_gmg_apply.argtypes = [P, P, P]
     lib.elas_pcg_gmg.restype = ctypes.c_int
     lib.elas_pcg_gmg.argtypes = [P, P, P, P, ctypes.c_double, ctypes.c_int, ctypes.POINTER(elas_solve_report), D]
+    lib.elas_set_deterministic.restype = ctypes.c_int
+    lib.elas_set_deterministic.argtypes = [P, ctypes.c_int]
     lib.elas_gmg_transfer.restype = ctypes.c_int
     lib.elas_gmg_transfer.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P]
     lib.elas_gmg_destroy.restype = None
@@ -288,6 +291,10 @@ def elas_launches_per_apply(h):
     return load().elas_launches_per_apply(h)
 
 
+def elas_set_deterministic(h, on):
+    _check(load().elas_set_deterministic(h, int(bool(on))), "elas_set_deterministic")
+
+
 def elas_diagonal(h, d):
     _check(load().elas_diagonal(h, _ptr(d)), "elas_diagonal")
 
@@ -405,6 +412,9 @@ class Operator:
 
     def diagonal(self, d):
         elas_diagonal(self.h, d)
+
+    def set_deterministic(self, on=True):
+        elas_set_deterministic(self.h, on)
 
     def chebyshev(self, order=3, alpha=0.1, beta=1.1, power_iters=10, v0=None, seed=0):
         c = Chebyshev(self, order, alpha, beta, power_iters, v0, seed)

@@ -440,3 +440,77 @@ def test_apply_host_chunked_pipeline(p, dims, faces):
     op.close()
     assert rel_l2(yh.numpy(), yd) <= 1e-15
     assert rel_l2(yh.numpy(), oracle.apply(oracle_mesh(P), P.x)) <= TOL
+
+
+# ---------------------------------------------------------------------------------------
+# deterministic (colored) scatter: bitwise reproducible applies
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("p,dims,faces,variant", [(2, (3, 4, 5), 1 | 32, 4), (6, (2, 3, 3), 0, 4), (4, (1, 1, 5), 63, 4),
+                                                  (3, (5, 2, 2), 8, 5), (8, (2, 2, 1), 2, 4), (1, (7, 3, 4), 16, 4)])
+def test_deterministic_colored_scatter(p, dims, faces, variant):
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_problem("t", *dims, p, p + 2, perturb=True, lognormal_material=True, faces=faces, seed=90 + p)
+    ys = []
+    for _ in range(2):
+        op = Operator.from_problem(P, variant=variant)
+        op.set_deterministic(True)
+        ys.append(gpu_apply(P, op=op))
+        ys.append(gpu_apply(P, op=op))
+        op.close()
+    assert all(np.array_equal(ys[0], v) for v in ys[1:])          # bitwise, across runs and ops
+    tol = TOL if variant == 4 else TOL_F32
+    assert rel_l2(ys[0], oracle.apply(oracle_mesh(P), P.x)) <= tol
+
+
+def test_deterministic_config4_and_slabs():
+    """Full-size config 4 p = 6 colored vs atomic (1e-14), and the colored slab loopback
+    (external-exchange mode, boundary layers) equal to the colored single-GPU apply bitwise."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_config(4, 6)
+    op = Operator.from_problem(P)
+    y_atomic = gpu_apply(P, op=op)
+    op.set_deterministic(True)
+    y_col = gpu_apply(P, op=op)
+    op.close()
+    assert rel_l2(y_col, y_atomic) <= 1e-14
+    P = synth.make_problem("t", 3, 3, 8, 3, 5, perturb=True, lognormal_material=True, faces=1, seed=5)
+    op = Operator.from_problem(P)
+    op.set_deterministic(True)
+    y_full = gpu_apply(P, op=op)
+    op.close()
+    Nx, Ny, Nz = P.node_dims
+    plane = Nx * Ny
+    xg = P.x.reshape(3, Nz, Ny, Nx)
+    ops, ys, ks = [], [], []
+    for r in range(3):
+        o = Operator.from_problem(P, rank=r, nranks=3)
+        o.set_deterministic(True)
+        b, e = o.zrange
+        xl = torch.from_numpy(np.ascontiguousarray(xg[:, b * P.p:e * P.p + 1])).cuda().reshape(-1)
+        yl = torch.empty_like(xl)
+        o.apply(xl, yl)
+        ops.append(o); ys.append(yl); ks.append((b * P.p, e * P.p))
+    torch.cuda.synchronize()
+    lo = [y.view(3, -1, plane)[:, 0].contiguous() for y in ys]
+    hi = [y.view(3, -1, plane)[:, -1].contiguous() for y in ys]
+    for r in range(3):
+        ops[r].interface_add(ys[r], hi[r - 1] if r > 0 else None, lo[r + 1] if r < 2 else None)
+    torch.cuda.synchronize()
+    yg = np.empty((3, Nz, plane))
+    for r in range(3):
+        yg[:, ks[r][0]:ks[r][1] + 1] = ys[r].view(3, -1, plane).cpu().numpy()
+        ops[r].close()
+    assert rel_l2(yg.reshape(-1), y_full) <= 1e-14
+
+
+def test_deterministic_only_folded():
+    torch_mod()
+    from paper_2601_08374_b200 import elas
+    P = synth.make_problem("t", 2, 2, 2, 6, 8, seed=1)
+    op = elas.Operator.from_problem(P, variant=elas.VARIANT_TENSOR)
+    with pytest.raises(elas.ElasError, match="folded"):
+        op.set_deterministic(True)
+    op.close()
