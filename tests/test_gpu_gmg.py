@@ -143,3 +143,24 @@ def test_gmg_errors():
     P = synth.make_problem("t", 3, 2, 2, 2, 3, seed=1)
     with pytest.raises(elas.ElasError, match="divisible"):
         elas.GMG.from_problem(P, levels=2)
+
+
+def test_fp64_pcg_with_fp32_vcycle():
+    """Mixed precision in the paper's solver: FP64 CG on the FP64 operator, V-cycle built from
+    ELAS_VARIANT_FOLDED_F32 operators; converges to the FP64 tolerance in about the same
+    number of iterations as the FP64 V-cycle."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import GMG, Operator, VARIANT_FOLDED_F32, elas_pcg_gmg
+    P = synth.make_problem("t", 8, 8, 8, 3, 5, perturb=True, lognormal_material=True, faces=1, seed=55)
+    op = Operator.from_problem(P)
+    g64 = GMG.from_problem(P, levels=3)
+    g32 = GMG.from_problem(P, levels=3, variant=VARIANT_FOLDED_F32)
+    b = torch.from_numpy(synth.splitmix_uniform(op.local_dofs, 12)).cuda()
+    x = torch.empty_like(b)
+    it64, c64, _, _ = elas_pcg_gmg(op.h, g64.h, b, x, 1e-10, 300)
+    it32, c32, r32, _ = elas_pcg_gmg(op.h, g32.h, b, x, 1e-10, 300)
+    assert c64 and c32 and r32 <= 1e-10 and it32 <= it64 + 3
+    Ax = torch.empty_like(b)
+    op.apply(x, Ax)
+    assert float(torch.linalg.norm(Ax - b) / torch.linalg.norm(b)) <= 1e-8
+    g32.close(); g64.close(); op.close()
