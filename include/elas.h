@@ -95,6 +95,9 @@ elas_op* elas_create(const elas_mesh* mesh, int p, int q, const double* lambda, 
  *                       arithmetic; x, y stay FP64 (converted on gather, FP64 atomics on
  *                       scatter).  Accuracy ~1e-6 relative, not the FP64 1e-12 (DESIGN.md
  *                       section 11); never chosen by AUTO.
+ *   ELAS_VARIANT_FOLDED_OTF  the folded FP64 kernel with GEOMETRY ON THE FLY: no stored
+ *                       quadrature data (40 doubles per element instead of 9 q^3); A~ rebuilt
+ *                       at every point from the trilinear map.
  *   ELAS_VARIANT_AUTO   the faster measured variant for (p, q).
  * The choice fixes the quadrature-data layout, so it is made at creation. */
 #define ELAS_VARIANT_AUTO 0
@@ -103,6 +106,7 @@ elas_op* elas_create(const elas_mesh* mesh, int p, int q, const double* lambda, 
 #define ELAS_VARIANT_THREAD 3
 #define ELAS_VARIANT_FOLDED 4
 #define ELAS_VARIANT_FOLDED_F32 5
+#define ELAS_VARIANT_FOLDED_OTF 6
 
 /* elas_create with an explicit kernel variant; NULL + ELAS_EINVAL message if the variant
  * does not exist for (p, q). */

@@ -47,7 +47,8 @@ DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
   cudaError_t apply_eo_info_p##P(int q, int fp32, ApplyLaunch* info);                            \
   cudaError_t apply_eo_launch_p##P(int q, int fp32, const Slab& s, const double* x, double* y,   \
                                    const void* qd, const double* rr, const void* tables,        \
-                                   int64_t e_begin, int64_t e_end, cudaStream_t st, const int* color);
+                                   int64_t e_begin, int64_t e_end, cudaStream_t st, const int* color, \
+                                   int otf);
 DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
 #undef DECL
 
@@ -89,9 +90,9 @@ cudaError_t apply_eo_info(int p, int q, int fp32, ApplyLaunch* info) {
 
 cudaError_t apply_eo_launch(int p, int q, int fp32, const Slab& s, const double* x, double* y, const void* qd,
                             const double* rr, const void* tables, int64_t e_begin, int64_t e_end,
-                            cudaStream_t st, const int* color) {
+                            cudaStream_t st, const int* color, int otf) {
   switch (p) {
-#define CASE(P) case P: return apply_eo_launch_p##P(q, fp32, s, x, y, qd, rr, tables, e_begin, e_end, st, color);
+#define CASE(P) case P: return apply_eo_launch_p##P(q, fp32, s, x, y, qd, rr, tables, e_begin, e_end, st, color, otf);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
     default: return cudaErrorInvalidValue;
@@ -205,8 +206,12 @@ int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* m
   const int n = p + 1;
   // tables = B | D | fold(B) | fold(D)  (the folded copies feed ELAS_VARIANT_FOLDED)
   const int fts = elas::fold_table_size(p, q);
-  std::vector<double> g(q), w(q), tabh(2 * q * n + 2 * fts);
+  std::vector<double> g(q), w(q), tabh(2 * q * n + 2 * fts + 2 * q);
   elas::host_tables(p, q, nullptr, g.data(), w.data(), tabh.data(), tabh.data() + q * n);
+  for (int a = 0; a < q; ++a) {   // Gauss points and sqrt weights (geometry-on-the-fly kernel)
+    tabh[elas::tables_gauss_offset(p, q, fts) + a] = g[a];
+    tabh[elas::tables_gauss_offset(p, q, fts) + q + a] = std::sqrt(w[a]);
+  }
   elas::host_fold_table(p, q, tabh.data(), tabh.data() + 2 * q * n);
   elas::host_fold_table(p, q, tabh.data() + q * n, tabh.data() + 2 * q * n + fts);
 
@@ -222,6 +227,7 @@ int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* m
   const int qlayout = op->variant == ELAS_VARIANT_TENSOR        ? elas::QD_LAYOUT_TC6
                       : op->variant == ELAS_VARIANT_THREAD      ? elas::QD_LAYOUT_E32
                       : op->variant == ELAS_VARIANT_FOLDED_F32 ? elas::QD_LAYOUT_LINES_F32
+                      : op->variant == ELAS_VARIANT_FOLDED_OTF ? elas::QD_LAYOUT_OTF
                                                                 : elas::QD_LAYOUT_LINES;
   op->qlayout = qlayout;
   const size_t qbytes = elas::qd_word_bytes(qlayout) * (size_t)elas::qd_stride(q, qlayout) * (size_t)elas::qd_elems(ne, qlayout);
@@ -299,7 +305,7 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
       const int cm[6] = {cx, cy, cz, ncx, ncy, iz0};
       e = elas::apply_eo_launch(op->p, op->q, op->variant == ELAS_VARIANT_FOLDED_F32, s, x, y, op->qd, op->rr,
                                 op->variant == ELAS_VARIANT_FOLDED_F32 ? (const void*)op->tabf : (const void*)op->tab,
-                                0, cnt, st, cm);
+                                0, cnt, st, cm, op->variant == ELAS_VARIANT_FOLDED_OTF);
     }
   } else
   e = op->variant == ELAS_VARIANT_TENSOR
@@ -310,6 +316,9 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
                       ? elas::apply_eo_launch(op->p, op->q, 0, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
                   : op->variant == ELAS_VARIANT_FOLDED_F32
                       ? elas::apply_eo_launch(op->p, op->q, 1, op->slab, x, y, op->qd, op->rr, op->tabf, e0, e1, st)
+                  : op->variant == ELAS_VARIANT_FOLDED_OTF
+                      ? elas::apply_eo_launch(op->p, op->q, 0, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st,
+                                              nullptr, 1)
                       : elas::apply_launch(op->p, op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st);
   if (e != cudaSuccess) return cuda_fail(e, "apply kernel launch");
   if (op->prof) CUDA_OR(cudaEventRecord(ev1, st), "cudaEventRecord");
@@ -387,7 +396,7 @@ elas_op* elas_create(const elas_mesh* m, int p, int q, const double* lambda, con
 
 elas_op* elas_create_ex(const elas_mesh* m, int p, int q, const double* lambda, const double* mu, int variant) {
   elas::g_err.clear();
-  if (variant < ELAS_VARIANT_AUTO || variant > ELAS_VARIANT_FOLDED_F32) {
+  if (variant < ELAS_VARIANT_AUTO || variant > ELAS_VARIANT_FOLDED_OTF) {
     set_error("elas_create_ex: unknown variant");
     return nullptr;
   }
@@ -508,7 +517,8 @@ int elas_variant(const elas_op* op) { return op ? op->variant : -1; }
 
 int elas_set_deterministic(elas_op* op, int on) {
   if (!op) { set_error("elas_set_deterministic: NULL op"); return ELAS_EINVAL; }
-  if (on && op->variant != ELAS_VARIANT_FOLDED && op->variant != ELAS_VARIANT_FOLDED_F32) {
+  if (on && op->variant != ELAS_VARIANT_FOLDED && op->variant != ELAS_VARIANT_FOLDED_F32 &&
+      op->variant != ELAS_VARIANT_FOLDED_OTF) {
     set_error("elas_set_deterministic: the colored scatter exists for the folded variants only");
     return ELAS_EINVAL;
   }

@@ -208,7 +208,19 @@ __device__ __forceinline__ void fold_in(const T (&u)[3][N], T (&up)[3][NE], T (&
   }
 }
 
-template <int P, int Q, typename T, bool COLORED>
+// OTF (geometry on the fly, FP64): no stored quadrature data; each stage-X thread rebuilds A~ at
+// its points from the element's trilinear-map coefficients (QD_LAYOUT_OTF, staged in shared
+// memory with the Gauss points and sqrt weights): along an x-line dx/dxi1 is constant and
+// dx/dxi2, dx/dxi3 are linear in xi1, so J costs 6 FMAs per point, then the adjugate, det and
+// one rsqrt: A~ = sqrt(mu) sqrt(w1 w2 w3) adj(J) / sqrt(det J)  (= sqrt(mu W) J^{-1}).
+template <int P, int Q, typename T>
+struct OtfSmem {
+  using C = CfgEO<P, Q, T>;
+  static constexpr int OFFG = (C::TAB + C::EB * (C::ZE + C::YE) + 1) & ~1;   // gq[Q] | sqw[Q] | geo[EB][GEO]
+  static constexpr size_t smem = sizeof(T) * (size_t)(OFFG + 2 * Q + C::EB * GEO_WORDS);
+};
+
+template <int P, int Q, typename T, bool COLORED, bool OTF = false>
 __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<P>::value : MinbEO<P>::value)
     apply_eo_kernel(const double* __restrict__ x, double* __restrict__ y, const T* __restrict__ qd,
                     const double* __restrict__ rr, const T* __restrict__ tables, Slab s,
@@ -218,7 +230,8 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   constexpr int N = C::N, NT = C::NT, EB = C::EB;
   constexpr int NE = F::NE, NH = F::NH, QE = F::QE, QH = F::QH, NHX = F::NHX;
   using RG = RingEO<P, Q, T>;
-  constexpr int R = RG::R;
+  constexpr int R = OTF ? 0 : RG::R;
+  constexpr bool STG = RG::STAGE && !OTF;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
   T* tB = smem;            // folded B (parity +1)
@@ -231,7 +244,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   const int tid = threadIdx.x;
   const int64_t e0 = e_begin + (int64_t)blockIdx.x * EB;
   const int ne = (int)((e_end - e0) < EB ? (e_end - e0) : EB);
-  if constexpr (RG::STAGE) {
+  if constexpr (STG) {
     if (tid == 0) {
       const uint32_t bar = smem_u32(mbar);
       const uint32_t bytes = (uint32_t)(sizeof(T) * ne * C::QDE);
@@ -297,10 +310,18 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
     const T* ft = tables + 2 * Q * N;   // fold(B) | fold(D) follow the plain tables
     for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = ft[t];
   }
+  if constexpr (OTF) {   // Gauss points, sqrt weights and the batch's Jacobian coefficients
+    T* gs = smem + OtfSmem<P, Q, T>::OFFG;
+    for (int t = tid; t < 2 * Q; t += NT) gs[t] = tables[2 * Q * N + 2 * F::TS + t];
+    for (int t = tid; t < ne * GEO_WORDS; t += NT) {
+      int gex, gey, gez;
+      gs[2 * Q + t] = qd[elem_coords<COLORED>(cm, s, e0 + t / GEO_WORDS, gex, gey, gez) * GEO_WORDS + t % GEO_WORDS];
+    }
+  }
 #if ELAS_L2_PREFETCH
   if (tid == 0 && pref_ctas > 0) {
     const int64_t pe0 = e0 + (int64_t)pref_ctas * EB;
-    if (pe0 < e_end && !COLORED) {
+    if (pe0 < e_end && !COLORED && !OTF) {   // (OTF: no quadrature data to prefetch)
       const int64_t pne = (e_end - pe0) < EB ? (e_end - pe0) : EB;
       const uintptr_t a0 = (uintptr_t)(qd + pe0 * (int64_t)C::QDE);
       const uintptr_t a1 = a0 + (uintptr_t)(pne * C::QDE * sizeof(T));
@@ -428,7 +449,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
 #pragma unroll
     for (int a1 = 0; a1 < R - 1; ++a1) ring_issue(a1);
   }
-  if constexpr (RG::STAGE) {
+  if constexpr (STG) {
     const uint32_t bar = smem_u32(mbar);
     asm volatile(
         "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(bar)
@@ -482,16 +503,57 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
       }
     }
     const T r = (T)__ldg(rr + e);
-    const T* qp = RG::STAGE ? sQ + el * C::QDE + L : qd + e * (int64_t)C::QDE + L;
+    const T* qp = STG ? sQ + el * C::QDE + L : qd + e * (int64_t)C::QDE + L;
+    // geometry on the fly: per-line constants
+    T col1[3], b2[3], s2[3], b3[3], s3[3], sq = 0;
+    const T* gs = smem + OtfSmem<P, Q, T>::OFFG;
+    if constexpr (OTF) {
+      const T* ge = gs + 2 * Q + el * GEO_WORDS;
+      const T xi2 = gs[a2], xi3 = gs[a3];
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        col1[m] = fma(fma(ge[9 + m], xi3, ge[3 + m]), xi2, fma(ge[6 + m], xi3, ge[m]));
+        b2[m] = fma(ge[18 + m], xi3, ge[12 + m]);
+        s2[m] = fma(ge[21 + m], xi3, ge[15 + m]);
+        b3[m] = fma(ge[30 + m], xi2, ge[24 + m]);
+        s3[m] = fma(ge[33 + m], xi2, ge[27 + m]);
+      }
+      sq = ge[36] * gs[Q + a2] * gs[Q + a3];
+    }
     T An[9];
-    if constexpr (R == 0) {
+    if constexpr (R == 0 && !OTF) {
 #pragma unroll
       for (int f = 0; f < 9; ++f) An[f] = qp[f * Q * Q];
     }
 #pragma unroll
     for (int a1 = 0; a1 < Q; ++a1) {
       T A[9];
-      if constexpr (R > 0) {
+      if constexpr (OTF) {
+        const T xi1 = gs[a1];
+        T J[3][3];
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+          J[m][0] = col1[m];
+          J[m][1] = fma(s2[m], xi1, b2[m]);
+          J[m][2] = fma(s3[m], xi1, b3[m]);
+        }
+        T adj[3][3];
+        adj[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+        adj[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+        adj[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+        adj[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+        adj[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+        adj[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+        adj[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+        adj[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+        adj[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        const T det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
+        const T sc = sq * gs[Q + a1] * rsqrt(det);
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int m = 0; m < 3; ++m) A[3 * d + m] = sc * adj[d][m];
+      } else if constexpr (R > 0) {
         if (a1 + R - 1 < Q) ring_issue(a1 + R - 1);
         else cp_async_commit();                    // empty group keeps the count uniform
         cp_async_wait<R - 1>();                    // this thread's copies of point a1 landed
@@ -505,7 +567,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
           for (int f = 0; f < 9; ++f) An[f] = qp[((a1 + 1) * 9 + f) * Q * Q];
         }
 #if ELAS_QD_L1PF > 0
-        if (!RG::STAGE && a1 + 1 + ELAS_QD_L1PF < Q) {   // L1 prefetch further ahead (no registers)
+        if (!STG && a1 + 1 + ELAS_QD_L1PF < Q) {   // L1 prefetch further ahead (no registers)
 #pragma unroll
           for (int f = 0; f < 9; ++f)
             asm volatile("prefetch.global.L1 [%0];" ::"l"(qp + ((a1 + 1 + ELAS_QD_L1PF) * 9 + f) * Q * Q));
@@ -711,29 +773,29 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   }
 }
 
-template <int P, int Q, typename T, bool COLORED>
+template <int P, int Q, typename T, bool COLORED, bool OTF = false>
 cudaError_t launch_apply_eo_pqc(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
                                 const void* tables, int64_t e_begin, int64_t e_end, cudaStream_t st,
                                 const ColorMap& cm) {
   using C = CfgEO<P, Q, T>;
-  using RG = RingEO<P, Q, T>;
+  constexpr size_t SMEM = OTF ? OtfSmem<P, Q, T>::smem : RingEO<P, Q, T>::smem;
   static bool attr_done = false;
   static int pref = -1;
   if (!attr_done) {
-    cudaError_t err = cudaFuncSetAttribute(apply_eo_kernel<P, Q, T, COLORED>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::smem);
+    cudaError_t err = cudaFuncSetAttribute(apply_eo_kernel<P, Q, T, COLORED, OTF>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     if (err != cudaSuccess) return err;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_eo_kernel<P, Q, T, COLORED>, C::NT, RG::smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_eo_kernel<P, Q, T, COLORED, OTF>, C::NT, SMEM);
     pref = sms * (per_sm > 0 ? per_sm : 1);
     attr_done = true;
   }
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
   const int64_t grid = (ne + C::EB - 1) / C::EB;
-  apply_eo_kernel<P, Q, T, COLORED><<<(unsigned)grid, C::NT, RG::smem, st>>>(
+  apply_eo_kernel<P, Q, T, COLORED, OTF><<<(unsigned)grid, C::NT, SMEM, st>>>(
       x, y, static_cast<const T*>(qd), rr, static_cast<const T*>(tables), s, e_begin, e_end, pref, cm);
   return cudaGetLastError();
 }
@@ -741,7 +803,12 @@ cudaError_t launch_apply_eo_pqc(const Slab& s, const double* x, double* y, const
 template <int P, int Q, typename T>
 cudaError_t launch_apply_eo_pq(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
                                const void* tables, int64_t e_begin, int64_t e_end, cudaStream_t st,
-                               const ColorMap& cm) {
+                               const ColorMap& cm, int otf) {
+  if constexpr (sizeof(T) == 8) {
+    if (otf)
+      return cm.on ? launch_apply_eo_pqc<P, Q, T, true, true>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm)
+                   : launch_apply_eo_pqc<P, Q, T, false, true>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm);
+  }
   return cm.on ? launch_apply_eo_pqc<P, Q, T, true>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm)
                : launch_apply_eo_pqc<P, Q, T, false>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm);
 }
@@ -767,15 +834,15 @@ void info_eo_pq(ApplyLaunch* info) {
   cudaError_t apply_eo_launch_p##P(int q, int fp32, const Slab& s, const double* x, double* y,  \
                                    const void* qd, const double* rr, const void* tables,        \
                                    int64_t e_begin, int64_t e_end, cudaStream_t st,             \
-                                   const int* color) {                                          \
+                                   const int* color, int otf) {                                 \
     ColorMap cm{0, 0, 0, 0, 0, 0, 0};                                                           \
     if (color) cm = ColorMap{1, color[0], color[1], color[2], color[3], color[4], color[5]};    \
     if (q == P + 1)                                                                             \
-      return fp32 ? launch_apply_eo_pq<P, P + 1, float>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm) \
-                  : launch_apply_eo_pq<P, P + 1, double>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm); \
+      return fp32 ? launch_apply_eo_pq<P, P + 1, float>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, 0) \
+                  : launch_apply_eo_pq<P, P + 1, double>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, otf); \
     if (q == P + 2)                                                                             \
-      return fp32 ? launch_apply_eo_pq<P, P + 2, float>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm) \
-                  : launch_apply_eo_pq<P, P + 2, double>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm); \
+      return fp32 ? launch_apply_eo_pq<P, P + 2, float>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, 0) \
+                  : launch_apply_eo_pq<P, P + 2, double>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, otf); \
     return cudaErrorInvalidValue;                                                               \
   }                                                                                             \
   }

@@ -37,9 +37,10 @@ int host_prolongation_1d(int p, double* M);
 cudaError_t apply_eo_info(int p, int q, int fp32, ApplyLaunch* info);
 // color == nullptr: elements [e_begin, e_end) with atomic scatter.  color = {cx, cy, cz, ncx, ncy,
 // iz0}: the linear range [e_begin, e_end) of one color's element lattice, plain-RMW scatter.
+// otf = 1: geometry on the fly (FP64 only; qd = geo[e][GEO_WORDS], QD_LAYOUT_OTF)
 cudaError_t apply_eo_launch(int p, int q, int fp32, const Slab& s, const double* x, double* y, const void* qd,
                             const double* rr, const void* tables, int64_t e_begin, int64_t e_end,
-                            cudaStream_t st, const int* color = nullptr);
+                            cudaStream_t st, const int* color = nullptr, int otf = 0);
 
 // Per-degree translation units (elas_apply_p<P>.cu) export these; q must be p+1 or p+2.
 // Returns cudaSuccess or an error; `info` only queries the configuration.
@@ -58,14 +59,24 @@ cudaError_t apply_tc_launch(const Slab& s, const double* x, double* y, const dou
 // 2 = lane-interleaved blocks of 32 elements for the one-thread-per-element p = 1 kernel:
 //     qd[e / 32][pt][f][e % 32], pt = a1 + q (a2 + q a3).
 // 3 = layout 0 in FP32 words (mixed-precision folded kernel), element stride rounded to 4 floats.
-enum { QD_LAYOUT_LINES = 0, QD_LAYOUT_TC6 = 1, QD_LAYOUT_E32 = 2, QD_LAYOUT_LINES_F32 = 3 };
+// 4 = geometry on the fly (ELAS_VARIANT_FOLDED_OTF): per element only the trilinear map's
+//     Jacobian coefficients, geo[e][GEO_WORDS]: dx/dxi1 = c0 + c1 xi2 + c2 xi3 + c3 xi2 xi3,
+//     dx/dxi2 = e0 + e1 xi1 + e2 xi3 + e3 xi1 xi3, dx/dxi3 = f0 + f1 xi1 + f2 xi2 + f3 xi1 xi2
+//     (3-vectors: c0..c3 at 0..11, e at 12..23, f at 24..35), sqrt(mu_e) at 36.
+enum { QD_LAYOUT_LINES = 0, QD_LAYOUT_TC6 = 1, QD_LAYOUT_E32 = 2, QD_LAYOUT_LINES_F32 = 3, QD_LAYOUT_OTF = 4 };
+constexpr int GEO_WORDS = 40;
 
 // qdata doubles per element: 9 q^3 rounded up to even so every element starts 16-B aligned
 // (TMA bulk copies need 16-B aligned addresses and sizes).
 constexpr int qd_stride_lines(int q) { return (9 * q * q * q + 1) & ~1; }
 inline int qd_stride(int q, int layout) {
-  return layout == QD_LAYOUT_LINES ? qd_stride_lines(q) : layout == QD_LAYOUT_LINES_F32 ? (9 * q * q * q + 3) & ~3 : 9 * q * q * q;
+  return layout == QD_LAYOUT_LINES       ? qd_stride_lines(q)
+         : layout == QD_LAYOUT_LINES_F32 ? (9 * q * q * q + 3) & ~3
+         : layout == QD_LAYOUT_OTF       ? GEO_WORDS
+                                         : 9 * q * q * q;
 }
+// op tables: B | D | fold(B) | fold(D) | Gauss points g[q] | sqrt(w)[q]
+inline int tables_gauss_offset(int p, int q, int fts) { return 2 * q * (p + 1) + 2 * fts; }
 inline size_t qd_word_bytes(int layout) { return layout == QD_LAYOUT_LINES_F32 ? 4 : 8; }
 // elements the qdata allocation must cover (E32 pads to whole blocks of 32)
 inline int64_t qd_elems(int64_t ne, int layout) { return layout == QD_LAYOUT_E32 ? (ne + 31) / 32 * 32 : ne; }

@@ -73,7 +73,34 @@ __global__ void qdata_kernel(int q, int layout, Slab s, const double* __restrict
     }
     const double W = qp.w[a1] * qp.w[a2] * qp.w[a3] * det;
     const double sc = sqrt(mu[e] * W) / det;   // A~ = sqrt(mu W) J^{-1} = sqrt(mu W) adj / det
-    if (layout == QD_LAYOUT_E32) {
+    if (layout == QD_LAYOUT_OTF) {   // geometry on the fly: the det check above at every point,
+      if (pt == 0) {                   // the Jacobian polynomial coefficients once per element
+        double Xv[2][2][2][3];
+        for (int c = 0; c < 2; ++c)
+          for (int b = 0; b < 2; ++b)
+            for (int a = 0; a < 2; ++a) {
+              const int64_t v = ((int64_t)(ez + c) * (s.ny + 1) + (ey + b)) * (s.nx + 1) + (ex + a);
+              for (int m = 0; m < 3; ++m) Xv[a][b][c][m] = V[v * 3 + m];
+            }
+        double* o = qd + e * (int64_t)GEO_WORDS;
+        for (int m = 0; m < 3; ++m) {
+          // d/dxi1: differences along a, bilinear in (xi2 = b, xi3 = c)
+          const double d00 = Xv[1][0][0][m] - Xv[0][0][0][m], d10 = Xv[1][1][0][m] - Xv[0][1][0][m];
+          const double d01 = Xv[1][0][1][m] - Xv[0][0][1][m], d11 = Xv[1][1][1][m] - Xv[0][1][1][m];
+          o[0 + m] = d00; o[3 + m] = d10 - d00; o[6 + m] = d01 - d00; o[9 + m] = d11 - d10 - d01 + d00;
+          // d/dxi2: differences along b, bilinear in (xi1 = a, xi3 = c)
+          const double g00 = Xv[0][1][0][m] - Xv[0][0][0][m], g10 = Xv[1][1][0][m] - Xv[1][0][0][m];
+          const double g01 = Xv[0][1][1][m] - Xv[0][0][1][m], g11 = Xv[1][1][1][m] - Xv[1][0][1][m];
+          o[12 + m] = g00; o[15 + m] = g10 - g00; o[18 + m] = g01 - g00; o[21 + m] = g11 - g10 - g01 + g00;
+          // d/dxi3: differences along c, bilinear in (xi1 = a, xi2 = b)
+          const double h00 = Xv[0][0][1][m] - Xv[0][0][0][m], h10 = Xv[1][0][1][m] - Xv[1][0][0][m];
+          const double h01 = Xv[0][1][1][m] - Xv[0][1][0][m], h11 = Xv[1][1][1][m] - Xv[1][1][0][m];
+          o[24 + m] = h00; o[27 + m] = h10 - h00; o[30 + m] = h01 - h00; o[33 + m] = h11 - h10 - h01 + h00;
+        }
+        o[36] = sqrt(mu[e]);
+        o[37] = o[38] = o[39] = 0.0;
+      }
+    } else if (layout == QD_LAYOUT_E32) {
       double* out = qd + (e >> 5) * (int64_t)(32 * 9 * q3) + (int64_t)pt * 9 * 32 + (e & 31);
       for (int d = 0; d < 3; ++d)
         for (int m = 0; m < 3; ++m) out[(3 * d + m) * 32] = sc * adj[d][m];

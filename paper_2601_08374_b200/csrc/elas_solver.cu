@@ -80,6 +80,32 @@ __device__ __forceinline__ int64_t qd_offset(int layout, int q, int64_t e, int a
   return e * es + (int64_t)a1 * 9 * q * q + a3 + q * a2;
 }
 
+// A~ at point (a1, a2, a3) from the geometry-on-the-fly coefficients (QD_LAYOUT_OTF)
+__device__ __forceinline__ void otf_A(const double* ge, const double* g, const double* sw, int a1, int a2, int a3,
+                                      double (&A)[9]) {
+  const double x1 = g[a1], x2 = g[a2], x3 = g[a3];
+  double J[3][3];
+  for (int m = 0; m < 3; ++m) {
+    J[m][0] = ge[m] + ge[3 + m] * x2 + ge[6 + m] * x3 + ge[9 + m] * x2 * x3;
+    J[m][1] = ge[12 + m] + ge[15 + m] * x1 + ge[18 + m] * x3 + ge[21 + m] * x1 * x3;
+    J[m][2] = ge[24 + m] + ge[27 + m] * x1 + ge[30 + m] * x2 + ge[33 + m] * x1 * x2;
+  }
+  double adj[3][3];
+  adj[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+  adj[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+  adj[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+  adj[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+  adj[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+  adj[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+  adj[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  adj[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+  adj[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  const double det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
+  const double sc = ge[36] * sw[a1] * sw[a2] * sw[a3] * rsqrt(det);
+  for (int d = 0; d < 3; ++d)
+    for (int m = 0; m < 3; ++m) A[3 * d + m] = sc * adj[d][m];
+}
+
 __global__ void diag_init_kernel(Slab s, double* __restrict__ d) {
   const int64_t n = 3 * s.nodes;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
@@ -89,7 +115,7 @@ __global__ void diag_init_kernel(Slab s, double* __restrict__ d) {
 // dynamic smem: B, D (q n each), F[3] (q n each), T0[3][q^3], T1[3][q^2 n], T2[3][q n^2], acc[3][n^3]
 __global__ void __launch_bounds__(128) diag_kernel(int p, int q, int layout, Slab s, const double* __restrict__ qd,
                                                    const double* __restrict__ rr, const double* __restrict__ tables,
-                                                   double* __restrict__ d) {
+                                                   const double* __restrict__ gauss, double* __restrict__ d) {
   extern __shared__ double sm[];
   const int n = p + 1, qn = q * n, q3 = q * q * q, n3 = n * n * n;
   double* sB = sm;
@@ -117,15 +143,24 @@ __global__ void __launch_bounds__(128) diag_kernel(int p, int q, int layout, Sla
     }
     for (int pt = tid; pt < q3; pt += NT) {
       const int a1 = pt % q, a2 = (pt / q) % q, a3 = pt / (q * q);
-      int fs;
-      const int64_t off = qd_offset(layout, q, e, a1, a2, a3, fs);
-      const float* qf = reinterpret_cast<const float*>(qd);
-      const bool f32 = layout == QD_LAYOUT_LINES_F32;
       double Ak[3], Al[3];
-      for (int m = 0; m < 3; ++m) {
-        const int64_t ik = off + (3 * k + m) * fs, il = off + (3 * l + m) * fs;
-        Ak[m] = f32 ? (double)qf[ik] : qd[ik];
-        Al[m] = f32 ? (double)qf[il] : qd[il];
+      if (layout == QD_LAYOUT_OTF) {
+        double A[9];
+        otf_A(qd + e * (int64_t)GEO_WORDS, gauss, gauss + q, a1, a2, a3, A);
+        for (int m = 0; m < 3; ++m) {
+          Ak[m] = A[3 * k + m];
+          Al[m] = A[3 * l + m];
+        }
+      } else {
+        int fs;
+        const int64_t off = qd_offset(layout, q, e, a1, a2, a3, fs);
+        const float* qf = reinterpret_cast<const float*>(qd);
+        const bool f32 = layout == QD_LAYOUT_LINES_F32;
+        for (int m = 0; m < 3; ++m) {
+          const int64_t ik = off + (3 * k + m) * fs, il = off + (3 * l + m) * fs;
+          Ak[m] = f32 ? (double)qf[ik] : qd[ik];
+          Al[m] = f32 ? (double)qf[il] : qd[il];
+        }
       }
       const double dot = Ak[0] * Al[0] + Ak[1] * Al[1] + Ak[2] * Al[2];
       for (int c = 0; c < 3; ++c) T0[c * q3 + pt] = r1 * Ak[c] * Al[c] + dot;
@@ -328,7 +363,8 @@ int diag_raw(elas_op* op, double* d) {
   }
   diag_init_kernel<<<grid_for(3 * s.nodes), 256, 0, op->stream>>>(s, d);
   const int64_t ne = (int64_t)s.nx * s.ny * s.nz;
-  if (ne > 0) diag_kernel<<<(unsigned)ne, 128, smem, op->stream>>>(p, q, op->qlayout, s, op->qd, op->rr, op->tab, d);
+  const double* gauss = op->tab + tables_gauss_offset(p, q, fold_table_size(p, q));
+  if (ne > 0) diag_kernel<<<(unsigned)ne, 128, smem, op->stream>>>(p, q, op->qlayout, s, op->qd, op->rr, op->tab, gauss, d);
   CK(cudaGetLastError(), "diagonal kernels");
   return exchange_planes(op, d);
 }

@@ -18,7 +18,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", os.environ.get("ELAS_LIBNAME", "libelas.so"))
 
-VARIANT_AUTO, VARIANT_SIMT, VARIANT_TENSOR, VARIANT_THREAD, VARIANT_FOLDED, VARIANT_FOLDED_F32 = 0, 1, 2, 3, 4, 5
+VARIANT_AUTO, VARIANT_SIMT, VARIANT_TENSOR, VARIANT_THREAD, VARIANT_FOLDED, VARIANT_FOLDED_F32, VARIANT_FOLDED_OTF = (
+    0, 1, 2, 3, 4, 5, 6)
 ELAS_OK, ELAS_EINVAL, ELAS_EGEOM, ELAS_ENOMEM, ELAS_ECUDA, ELAS_ENCCL = 0, -1, -2, -3, -4, -5
 FACE_XMIN, FACE_XMAX, FACE_YMIN, FACE_YMAX, FACE_ZMIN, FACE_ZMAX = 1, 2, 4, 8, 16, 32
 
