@@ -177,14 +177,15 @@ int elas_profile_read(elas_op* op, double* apply_kernel_ms, int64_t* launches);
  * leaves partial planes for elas_interface_add).  ELAS_OK / ELAS_EINVAL / ELAS_ECUDA. */
 int elas_diagonal(elas_op* op, double* d);
 
-/* Chebyshev smoother on D^{-1} A (D = elas_diagonal), single-GPU operators (nranks == 1).
+/* Chebyshev smoother on D^{-1} A (D = elas_diagonal), single-GPU operators or NCCL slab mode
+ * (dots allreduced; external-exchange ops are rejected).
  * Create: computes and caches D^{-1} in the op, runs `power_iters` power iterations
  *   v <- v/|v|; w = D^{-1} A v; lam = v.w; v <- w/|w|
  * from v0 (DEVICE, NULL => splitmix64 counter generator with `seed`, the same generator as
  * synth.splitmix_uniform) and sets lam_max = 1.1 lam.  The polynomial is the degree-`order`
  * Chebyshev polynomial for the interval [alpha lam_max, beta lam_max] (SPEC defaults 3, 0.1,
  * 1.1).  NULL + ELAS_EINVAL message on bad arguments (order < 1, !(0 < alpha < beta),
- * power_iters < 1, nranks > 1) or a non-positive estimate.  Owns 3 work vectors. */
+ * power_iters < 1, external-exchange op) or a non-positive estimate.  Owns 3 work vectors. */
 typedef struct elas_cheb elas_cheb;
 elas_cheb* elas_cheb_create(elas_op* op, int order, double alpha, double beta, int power_iters, const double* v0,
                             unsigned long long seed);
@@ -195,7 +196,7 @@ double elas_cheb_lambda_max(const elas_cheb* ch);
 int elas_cheb_apply(elas_cheb* ch, const double* b, double* x);
 void elas_cheb_destroy(elas_cheb* ch);   /* NULL-safe; synchronises the op's stream */
 
-/* Preconditioned conjugate gradients from x = 0 (single-GPU operators).  precond:
+/* Preconditioned conjugate gradients from x = 0 (single GPU or NCCL slab mode).  precond:
  * ELAS_PC_NONE, ELAS_PC_JACOBI (D^{-1}, cached in the op) or ELAS_PC_CHEBYSHEV (z =
  * p_k(D^{-1}A) D^{-1} r with `cheb`'s operator, which may be another op of the same mesh and
  * stream -- e.g. an ELAS_VARIANT_FOLDED_F32 op: FP64 CG with a mixed-precision smoother).  Stops when sqrt(r.z / r0.z0) <= rtol or after
@@ -213,6 +214,12 @@ typedef struct {
 } elas_solve_report;
 int elas_pcg(elas_op* op, int precond, elas_cheb* cheb, const double* b, double* x, double rtol, int maxit,
              elas_solve_report* report, double* history);
+
+/* Distributed dot product a.b over the dofs this rank OWNS (the lower interface plane of a slab
+ * belongs to the rank below), allreduced over the communicator in NCCL mode; in external-
+ * exchange mode the rank-local partial (the caller sums them).  Synchronises; result on the
+ * host.  This is the reduction elas_pcg and the power iteration use. */
+int elas_dot(elas_op* op, const double* a, const double* b, double* result);
 
 /* Geometric multigrid V-cycle (Sec. 3, Fig. 2),
  * single-GPU (nranks == 1).  Readings R22-R25 in DESIGN.md.

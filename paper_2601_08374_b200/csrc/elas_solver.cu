@@ -204,13 +204,21 @@ __global__ void __launch_bounds__(128) diag_kernel(int p, int q, int layout, Sla
 
 // partial[b] = sum over this block's grid-stride share of w_i a_i b_i (w_i = 0 on interface
 // planes owned by the rank below; none for one rank)
+// partial[b] = this block's share of sum_c sum_{node >= skip} a b over the 3 components.  skip =
+// one node plane on ranks > 0 of a slab partition: the lower interface plane is replicated and
+// owned by the rank below, so every dof is counted once in the allreduced dot.
 __global__ void __launch_bounds__(RED_THREADS) dot_partial_kernel(const double* __restrict__ a,
-                                                                  const double* __restrict__ b, int64_t n,
-                                                                  double* __restrict__ partial) {
+                                                                  const double* __restrict__ b, int64_t nodes,
+                                                                  int64_t skip, double* __restrict__ partial) {
   __shared__ double sh[RED_THREADS];
   double v = 0.0;
-  for (int64_t t = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x; t < n; t += (int64_t)RED_BLOCKS * RED_THREADS)
-    v = fma(a[t], b[t], v);
+  for (int c = 0; c < 3; ++c) {
+    const double* ac = a + c * nodes;
+    const double* bc = b + c * nodes;
+    for (int64_t t = skip + blockIdx.x * (int64_t)RED_THREADS + threadIdx.x; t < nodes;
+         t += (int64_t)RED_BLOCKS * RED_THREADS)
+      v = fma(ac[t], bc[t], v);
+  }
   sh[threadIdx.x] = v;
   __syncthreads();
   for (int w = RED_THREADS / 2; w > 0; w >>= 1) {
@@ -234,10 +242,23 @@ __global__ void __launch_bounds__(RED_THREADS) dot_final_kernel(const double* __
   if (threadIdx.x == 0) *out = sh[0];
 }
 
-int dot(const double* a, const double* b, int64_t n, double* red, int slot, cudaStream_t st) {
-  dot_partial_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, b, n, red);
-  dot_final_kernel<<<1, RED_THREADS, 0, st>>>(red, red + RED_BLOCKS + slot);
+// distributed dot over the owned dofs of this rank, result in the device scalar `slot`
+// (allreduced over the slab communicator in NCCL mode)
+int dot(elas_op* op, const double* a, const double* b, int slot) {
+  const Slab& s = op->slab;
+  cudaStream_t st = op->stream;
+  const int64_t skip = op->rank > 0 ? (int64_t)s.Nx * s.Ny : 0;
+  dot_partial_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, b, s.nodes, skip, op->red);
+  dot_final_kernel<<<1, RED_THREADS, 0, st>>>(op->red, op->red + RED_BLOCKS + slot);
   CK(cudaGetLastError(), "dot kernels");
+  if (op->comm) {
+    ncclResult_t r = ncclAllReduce(op->red + RED_BLOCKS + slot, op->red + RED_BLOCKS + slot, 1, ncclDouble, ncclSum,
+                                   op->comm, st);
+    if (r != ncclSuccess) {
+      set_error(std::string("ncclAllReduce (dot): ") + ncclGetErrorString(r));
+      return ELAS_ENCCL;
+    }
+  }
   return ELAS_OK;
 }
 
@@ -384,8 +405,9 @@ int ensure_dinv(elas_op* op) {
 }
 
 bool solver_ok(const elas_op* op, const char* who) {
-  if (op->nranks != 1) {
-    set_error(std::string(who) + ": the solver layer supports single-GPU operators only (nranks == 1)");
+  if (op->nranks != 1 && !op->comm) {
+    set_error(std::string(who) + ": distributed solvers need the NCCL slab mode (external-exchange ops "
+              "cannot reduce dots)");
     return false;
   }
   return true;
@@ -449,7 +471,7 @@ int pcg_core(elas_op* op, int kind, const PrecondFn& M, const double* b, double*
     CK(cudaMemcpyAsync(z, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
   }
   CK(cudaGetLastError(), "preconditioner kernel");
-  if ((rc = dot(r, z, n, op->red, S_RZ, st))) return rc;
+  if ((rc = dot(op, r, z, S_RZ))) return rc;
   double rz0 = 1.0;
   if (check) {
     if ((rc = read_scalar(op, S_RZ, &rz0))) return rc;
@@ -462,12 +484,12 @@ int pcg_core(elas_op* op, int kind, const PrecondFn& M, const double* b, double*
     pcg_direction_kernel<<<g, 256, 0, st>>>(p, z, S, n, 1);
     while (it < maxit) {
       if ((rc = elas_apply(op, p, t))) return rc;
-      if ((rc = dot(p, t, n, op->red, S_PT, st))) return rc;
+      if ((rc = dot(op, p, t, S_PT))) return rc;
       pcg_update_kernel<<<g, 256, 0, st>>>(x, r, fused_z ? z : nullptr, p, t,
                                            kind == ELAS_PC_JACOBI ? op->dinv : nullptr, S, n);
       CK(cudaGetLastError(), "pcg update kernel");
       if (!fused_z && (rc = M(r, z))) return rc;
-      if ((rc = dot(r, z, n, op->red, S_RZNEW, st))) return rc;
+      if ((rc = dot(op, r, z, S_RZNEW))) return rc;
       ++it;
       if (check) {
         double rz = 0.0;
@@ -534,12 +556,12 @@ elas_cheb* elas_cheb_create(elas_op* op, int order, double alpha, double beta, i
   if (v0) e = cudaMemcpyAsync(w, v0, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
   else elas::splitmix_kernel<<<g, 256, 0, st>>>(w, n, seed);
   if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return bail(e, "power iteration start vector");
-  if (elas::dot(w, w, n, op->red, elas::S_NRM, st)) return bail(cudaSuccess, "");
+  if (elas::dot(op, w, w, elas::S_NRM)) return bail(cudaSuccess, "");
   elas::normalize_kernel<<<g, 256, 0, st>>>(v, w, S + elas::S_NRM, n);
   for (int it = 0; it < power_iters; ++it) {
     if (elas_apply(op, v, t)) return bail(cudaSuccess, "");
     elas::scale_kernel<<<g, 256, 0, st>>>(w, op->dinv, t, n);
-    if (elas::dot(v, w, n, op->red, elas::S_LAM, st) || elas::dot(w, w, n, op->red, elas::S_NRM, st))
+    if (elas::dot(op, v, w, elas::S_LAM) || elas::dot(op, w, w, elas::S_NRM))
       return bail(cudaSuccess, "");
     elas::normalize_kernel<<<g, 256, 0, st>>>(v, w, S + elas::S_NRM, n);
   }
@@ -586,6 +608,14 @@ int elas_pcg(elas_op* op, int precond, elas_cheb* cheb, const double* b, double*
                           [cheb](const double* r, double* z) { return elas::cheb_run(cheb, r, z, true); }, b, x,
                           rtol, maxit, true, rep, history);
   return elas::pcg_core(op, precond, elas::PrecondFn(), b, x, rtol, maxit, true, rep, history);
+}
+
+int elas_dot(elas_op* op, const double* a, const double* b, double* result) {
+  if (!op || !a || !b || !result) { elas::set_error("elas_dot: NULL argument"); return ELAS_EINVAL; }
+  int rc;
+  if ((rc = elas::ensure_red(op))) return rc;
+  if ((rc = elas::dot(op, a, b, elas::S_DOT))) return rc;
+  return elas::read_scalar(op, elas::S_DOT, result);
 }
 
 }  // extern "C"

@@ -30,7 +30,7 @@ EXPORTED = ["elas_create", "elas_apply", "elas_apply_host", "elas_interface_add"
             "elas_diagonal", "elas_cheb_create", "elas_cheb_lambda_max", "elas_cheb_apply",
             "elas_cheb_destroy", "elas_pcg", "elas_gmg_create", "elas_gmg_level_op", "elas_gmg_levels",
             "elas_gmg_set_stream", "elas_gmg_apply", "elas_pcg_gmg", "elas_gmg_destroy", "elas_gmg_transfer",
-            "elas_set_deterministic"]
+            "elas_set_deterministic", "elas_dot"]
 PC_NONE, PC_JACOBI, PC_CHEBYSHEV = 0, 1, 2
 
 
@@ -129,6 +129,8 @@ def load(path=None):
     lib.elas_gmg_apply.argtypes = [P, P, P]
     lib.elas_pcg_gmg.restype = ctypes.c_int
     lib.elas_pcg_gmg.argtypes = [P, P, P, P, ctypes.c_double, ctypes.c_int, ctypes.POINTER(elas_solve_report), D]
+    lib.elas_dot.restype = ctypes.c_int
+    lib.elas_dot.argtypes = [P, P, P, D]
     lib.elas_set_deterministic.restype = ctypes.c_int
     lib.elas_set_deterministic.argtypes = [P, ctypes.c_int]
     lib.elas_gmg_transfer.restype = ctypes.c_int
@@ -290,6 +292,12 @@ def elas_profile_read(h):
 
 def elas_launches_per_apply(h):
     return load().elas_launches_per_apply(h)
+
+
+def elas_dot(h, a, b):
+    out = ctypes.c_double(0.0)
+    _check(load().elas_dot(h, _ptr(a), _ptr(b), ctypes.byref(out)), "elas_dot")
+    return out.value
 
 
 def elas_set_deterministic(h, on):

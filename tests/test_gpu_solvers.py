@@ -106,6 +106,7 @@ def test_default_start_vector_is_splitmix():
     from paper_2601_08374_b200.elas import Operator
     P = small_problem(2, seed=31)
     op = Operator.from_problem(P)
+    op.set_deterministic(True)     # atomics would make the two estimates differ in the last bit
     a = op.chebyshev(power_iters=4, seed=123).lambda_max
     v0 = torch.from_numpy(synth.splitmix_uniform(P.num_dofs, 123)).cuda()
     b = op.chebyshev(power_iters=4, v0=v0).lambda_max
@@ -204,7 +205,7 @@ def test_solver_error_paths():
     with pytest.raises(elas.ElasError, match="alpha"):
         op.chebyshev(alpha=0.5, beta=0.4)
     op2 = elas.Operator.from_problem(P, rank=0, nranks=2)
-    with pytest.raises(elas.ElasError, match="single-GPU"):
+    with pytest.raises(elas.ElasError, match="NCCL slab mode"):
         op2.chebyshev()
     op2.close()
     op.close()
@@ -232,3 +233,30 @@ def test_pcg_fp64_with_fp32_chebyshev():
     op.apply(x, Ax)
     assert float(torch.linalg.norm(Ax - b) / torch.linalg.norm(b)) <= 1e-7
     ch32.close(); ch64.close(); op32.close(); op.close()
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 5])
+def test_distributed_dot_ownership(nranks):
+    """elas_dot on slab operators counts every replicated interface plane once: the sum of the
+    rank-local partials (external-exchange mode, one GPU) equals the single-operator dot."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator, elas_dot
+    P = synth.make_problem("t", 3, 2, 10, 3, 5, perturb=True, seed=70 + nranks)
+    n = P.num_dofs
+    a = synth.splitmix_uniform(n, 1)
+    b = synth.splitmix_uniform(n, 2)
+    op = Operator.from_problem(P)
+    full = elas_dot(op.h, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    op.close()
+    assert abs(full - float(a @ b)) <= 1e-12 * abs(float(np.abs(a) @ np.abs(b)))
+    Nx, Ny, Nz = P.node_dims
+    ag, bg = a.reshape(3, Nz, Ny * Nx), b.reshape(3, Nz, Ny * Nx)
+    tot = 0.0
+    for r in range(nranks):
+        o = Operator.from_problem(P, rank=r, nranks=nranks)
+        z0, z1 = o.zrange
+        al = torch.from_numpy(np.ascontiguousarray(ag[:, z0 * P.p:z1 * P.p + 1])).cuda().reshape(-1)
+        bl = torch.from_numpy(np.ascontiguousarray(bg[:, z0 * P.p:z1 * P.p + 1])).cuda().reshape(-1)
+        tot += elas_dot(o.h, al, bl)
+        o.close()
+    assert abs(tot - full) <= 1e-12 * abs(float(np.abs(a) @ np.abs(b)))
