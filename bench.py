@@ -246,6 +246,45 @@ def sweep_config4(reps=10, warmup=3, variant=0, ps=range(1, 9)):
     return out
 
 
+# ------------------------------------------------------------------------------ config 2 hot / cold
+
+def config2_hot_cold(reps=20):
+    """Config 2 (823,875 DoF; 77 MB working set < 126 MB L2): back-to-back applies (hot) and
+    applies each preceded by a 2 x L2 memset (cold), per SURVEY 8(d)."""
+    import torch
+    import synth
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_config(2)
+    op = Operator.from_problem(P)
+    x = torch.from_numpy(P.x).cuda()
+    y = torch.empty_like(x)
+    flush = torch.empty(2 * 126 * 2 ** 20 // 4, dtype=torch.int32, device="cuda")
+    for _ in range(5):
+        op.apply(x, y)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        op.apply(x, y)
+    b.record()
+    torch.cuda.synchronize()
+    hot = a.elapsed_time(b) / reps
+    cold = []
+    for _ in range(reps):
+        flush.zero_()
+        a.record()
+        op.apply(x, y)
+        b.record()
+        torch.cuda.synchronize()
+        cold.append(a.elapsed_time(b))
+    cold.sort()
+    op.close()
+    return {"workload": "cfg2: 16^3 hexes, Q4 q=6, perturbed, 823875 DoF", "hot_ms": round(hot, 4),
+            "hot_gdofs": round(P.num_dofs / hot / 1e6, 3), "cold_median_ms": round(cold[len(cold) // 2], 4),
+            "cold_gdofs": round(P.num_dofs / cold[len(cold) // 2] / 1e6, 3),
+            "note": "cold = 2 x L2 memset before each individually timed apply"}
+
+
 # ------------------------------------------------------------------------------ solver row
 
 def solver_bench(cfg=3, passes=10, rtol=1e-8, maxit=4000):
@@ -397,6 +436,19 @@ def run_ours(args):
     ms_per_step = t_ms / args.steps
     value = P.num_dofs / (ms_per_step / 1e3) / 1e9
 
+    # per-apply distribution (SURVEY 8(d) timing protocol): one event pair per apply, separate
+    # from the timed region above
+    per = []
+    pe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(min(args.steps, 10))]
+    for a_, b_ in pe:
+        a_.record(stream)
+        op.apply(x, y)
+        b_.record(stream)
+    torch.cuda.synchronize()
+    per = sorted(a_.elapsed_time(b_) for a_, b_ in pe)
+    per_apply = {"median_ms": round(per[len(per) // 2], 4), "min_ms": round(per[0], 4), "max_ms": round(per[-1], 4),
+                 "n": len(per)}
+
     # the bitwise-reproducible colored scatter (elas_set_deterministic): same op, same inputs
     det = None
     if op.variant in (4, 5):
@@ -490,6 +542,7 @@ def run_ours(args):
                     "note": "elas_apply_host: pinned host x -> device, apply, device -> pinned host y"},
             "gpu_launches": launches,
             "roofline": roof,
+            "per_apply": per_apply,
             "deterministic": det,
             "geometry_on_the_fly": otf,
             "setup_s": round(setup_s, 3), "x_generation_s": round(t_gen, 2)}
@@ -498,6 +551,8 @@ def run_ours(args):
     torch.cuda.empty_cache()
     if ws == 1 and rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(P)
+    if ws == 1 and not args.no_sweep:
+        line["config2_hot_cold"] = config2_hot_cold()
     if ws == 1 and not args.no_solver:
         line["solver"] = solver_bench()
     if ws == 1 and not args.no_sweep:
