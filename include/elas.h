@@ -154,7 +154,9 @@ int elas_local_zrange(const elas_op* op, int32_t* ez_begin, int32_t* ez_end);
 /* Make subsequent applies run on `cuda_stream` (a cudaStream_t; NULL = legacy default). */
 int elas_set_stream(elas_op* op, void* cuda_stream);
 
-/* Number of kernel launches one elas_apply issues (for the bench's launch accounting). */
+/* Number of kernel launches one elas_apply issues (for the bench's launch accounting): the fused
+ * apply (8 in colored mode, per element range), the Dirichlet-face copy when faces are
+ * constrained, and the interface plane adds in NCCL mode; the y memset is not a kernel. */
 int elas_launches_per_apply(const elas_op* op);
 
 /* Measurement hook (used by bench.py): enabling starts a fresh window; while enabled, every launch of the fused apply

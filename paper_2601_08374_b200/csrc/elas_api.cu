@@ -526,15 +526,35 @@ int elas_set_deterministic(elas_op* op, int on) {
   return ELAS_OK;
 }
 
+// kernels of ONE element range [z0, z1) of layers: 1, or the non-empty colors in colored mode
+static int range_launches(const elas_op* op, int z0, int z1) {
+  if (z1 <= z0) return 0;
+  if (!op->deterministic) return 1;
+  const Slab& s = op->slab;
+  int n = 0;
+  for (int c = 0; c < 8; ++c) {
+    const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
+    const int ncx = (s.nx - cx + 1) / 2, ncy = (s.ny - cy + 1) / 2;
+    const int iz0 = (z0 - cz + 1) / 2 > 0 ? (z0 - cz + 1) / 2 : 0;
+    const int iz1 = (z1 - cz + 1) / 2 > 0 ? (z1 - cz + 1) / 2 : 0;
+    if ((int64_t)ncx * ncy * (iz1 > iz0 ? iz1 - iz0 : 0) > 0) ++n;
+  }
+  return n;
+}
+
 int elas_launches_per_apply(const elas_op* op) {
   if (!op) return -1;
-  if (op->nranks == 1 || op->external) return 2;  // init + apply
+  // init = a memset (not a kernel) + the Dirichlet-face copy kernel when faces are constrained
+  int n = op->slab.faces ? 1 : 0;
   const int nzl = op->ez1 - op->ez0;
+  if (op->nranks == 1 || op->external) return n + range_launches(op, 0, nzl);
   const bool lo = op->rank > 0, hi = op->rank < op->nranks - 1;
-  int n = 1;                                       // init
-  if (lo && hi && nzl > 1) n += 2; else n += 1;    // boundary layer(s)
-  if (nzl - (int)lo - (int)hi > 0) n += 1;         // interior
-  n += (int)lo + (int)hi;                          // plane adds
+  int i0 = 0, i1 = nzl;
+  if (lo) { n += range_launches(op, 0, 1); i0 = 1; }
+  if (hi && nzl - 1 >= i0) { n += range_launches(op, nzl - 1, nzl); i1 = nzl - 1; }
+  else if (hi) i1 = i0;
+  n += range_launches(op, i0, i1);             // interior
+  n += (int)lo + (int)hi;                      // plane adds
   return n;
 }
 

@@ -551,3 +551,25 @@ def test_folded_otf_config5_sampled():
     op.close()
     rows = sample_rows(P, 256, 15, extra=plane_rows(P, 128 * P.p, 8, 3))
     assert rel_l2(y[rows], oracle.apply_rows(oracle_mesh(P), P.x, rows)) <= TOL
+
+
+def test_launches_per_apply_matches_profiler():
+    """elas_launches_per_apply equals the kernels torch's profiler sees for one apply."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    from torch.profiler import profile, ProfilerActivity
+    for faces, det in [(0, False), (1, False), (1, True), (0, True)]:
+        P = synth.make_problem("t", 4, 3, 5, 3, 5, perturb=True, faces=faces, seed=9)
+        op = Operator.from_problem(P)
+        op.set_deterministic(det)
+        x = torch.from_numpy(P.x).cuda()
+        y = torch.empty_like(x)
+        op.apply(x, y)
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            op.apply(x, y)
+            torch.cuda.synchronize()
+        kernels = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
+                   and "Memset" not in e.name and "memset" not in e.name]
+        assert len(kernels) == op.launches_per_apply, (faces, det, [k.name for k in kernels])
+        op.close()
