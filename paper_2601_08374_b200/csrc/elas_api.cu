@@ -227,7 +227,7 @@ int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* m
   const int qlayout = op->variant == ELAS_VARIANT_TENSOR        ? elas::QD_LAYOUT_TC6
                       : op->variant == ELAS_VARIANT_THREAD      ? elas::QD_LAYOUT_E32
                       : op->variant == ELAS_VARIANT_FOLDED_F32 ? elas::QD_LAYOUT_LINES_F32
-                      : op->variant == ELAS_VARIANT_FOLDED_OTF ? elas::QD_LAYOUT_OTF
+                      : op->variant == ELAS_VARIANT_FOLDED_OTF ? (p == 1 ? elas::QD_LAYOUT_OTF32 : elas::QD_LAYOUT_OTF)
                                                                 : elas::QD_LAYOUT_LINES;
   op->qlayout = qlayout;
   const size_t qbytes = elas::qd_word_bytes(qlayout) * (size_t)elas::qd_stride(q, qlayout) * (size_t)elas::qd_elems(ne, qlayout);
@@ -316,6 +316,8 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
                       ? elas::apply_eo_launch(op->p, op->q, 0, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
                   : op->variant == ELAS_VARIANT_FOLDED_F32
                       ? elas::apply_eo_launch(op->p, op->q, 1, op->slab, x, y, op->qd, op->rr, op->tabf, e0, e1, st)
+                  : (op->variant == ELAS_VARIANT_FOLDED_OTF && op->p == 1)   // thread-per-element kernel
+                      ? elas::apply_p1t_launch(op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st, 1)
                   : op->variant == ELAS_VARIANT_FOLDED_OTF
                       ? elas::apply_eo_launch(op->p, op->q, 0, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st,
                                               nullptr, 1)

@@ -315,7 +315,11 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
     for (int t = tid; t < 2 * Q; t += NT) gs[t] = tables[2 * Q * N + 2 * F::TS + t];
     for (int t = tid; t < ne * GEO_WORDS; t += NT) {
       int gex, gey, gez;
-      gs[2 * Q + t] = qd[elem_coords<COLORED>(cm, s, e0 + t / GEO_WORDS, gex, gey, gez) * GEO_WORDS + t % GEO_WORDS];
+      const int64_t ge = elem_coords<COLORED>(cm, s, e0 + t / GEO_WORDS, gex, gey, gez);
+      const int w = t % GEO_WORDS;
+      // p = 1 ops store the geometry lane-interleaved for the thread-per-element kernel (OTF32)
+      gs[2 * Q + t] = P == 1 ? qd[(ge >> 5) * (int64_t)(32 * GEO_WORDS) + w * 32 + (ge & 31)]
+                             : qd[ge * GEO_WORDS + w];
     }
   }
 #if ELAS_L2_PREFETCH

@@ -53,17 +53,22 @@ __device__ __forceinline__ void pointwise(double (&G)[3][3], const double (&A)[9
       G[c][d] = fma(S[c][2], A[3 * d + 2], fma(S[c][1], A[3 * d + 1], S[c][0] * A[3 * d]));
 }
 
-template <int Q>
+// OTF: geometry on the fly (ELAS_VARIANT_FOLDED_OTF at p = 1): qd = geo32 (QD_LAYOUT_OTF32, 40 words
+// per element, lane-interleaved); each thread reads its element's Jacobian/material words per
+// x-line (L1-resident after the first) and rebuilds A~ = sqrt(mu) sqrt(w1 w2 w3) adj(J) / sqrt(det)
+// at every point: the HBM stream of 9 q^3 doubles per element that bounds this kernel disappears.
+template <int Q, bool OTF>
 __global__ void __launch_bounds__(NT, ELAS_P1T_MINB)
     apply_p1_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
                     const double* __restrict__ rr, const double* __restrict__ tables, Slab s,
-                    int64_t e_begin, int64_t e_end, int pref_ctas) {
+                    int64_t e_begin, int64_t e_end, int pref_ctas, const double* __restrict__ gauss) {
   constexpr int N = 2;
-  __shared__ double tb[2 * Q * N];  // B then D (q x 2): broadcast reads
+  __shared__ double tb[2 * Q * N + 2 * Q];  // B then D (q x 2): broadcast reads; OTF: g[q], sqrt(w)[q]
   __shared__ double su[24 * NT];     // gathered element vectors, one column per thread
   if (threadIdx.x < 2 * Q * N) tb[threadIdx.x] = tables[threadIdx.x];
+  if (OTF && threadIdx.x < 2 * Q) tb[2 * Q * N + threadIdx.x] = gauss[threadIdx.x];
 #if ELAS_L2_PREFETCH
-  if (threadIdx.x == 0 && pref_ctas > 0) {
+  if (!OTF && threadIdx.x == 0 && pref_ctas > 0) {
     const int64_t pe0 = e_begin + ((int64_t)blockIdx.x + pref_ctas) * NT;
     if (pe0 < e_end) {
       const int64_t pne = (e_end - pe0) < NT ? (e_end - pe0) : NT;
@@ -110,6 +115,10 @@ __global__ void __launch_bounds__(NT, ELAS_P1T_MINB)
   const double r = __ldg(rr + e);
   const int lane = (int)(e & 31);
   const double* qb = qd + (e >> 5) * (int64_t)(32 * 9 * Q * Q * Q) + lane;
+  // OTF: this element's geometry words, read per line through L1 (coalesced, lane-interleaved)
+  const double* gcol = qd + (e >> 5) * (int64_t)(32 * GEO_WORDS) + lane;
+  constexpr int GS = 32;
+  const double* gq = tb + 2 * Q * N;   // Gauss points, then sqrt weights (OTF)
 
 #pragma unroll 1
   for (int a3 = 0; a3 < Q; ++a3)
@@ -140,13 +149,57 @@ __global__ void __launch_bounds__(NT, ELAS_P1T_MINB)
 #pragma unroll
           for (int a1 = 0; a1 < Q; ++a1) G[a1][c][d] = fma(cx[a1 * N + 1], T[1], cx[a1 * N] * T[0]);
         }
+      if constexpr (OTF) {
+        // per line: dx/dxi1 constant, dx/dxi2 and dx/dxi3 linear in xi1
+        const double xi2 = gq[a2], xi3 = gq[a3];
+        double col1[3], b2[3], s2[3], b3[3], s3[3];
 #pragma unroll
-      for (int a1 = 0; a1 < Q; ++a1) {
-        const double* q = qb + (int64_t)((a1 + Q * (a2 + Q * a3)) * 9) * 32;
-        double A[9];
+        for (int m = 0; m < 3; ++m) {
+          col1[m] = fma(fma(__ldg(gcol + (9 + m) * GS), xi3, __ldg(gcol + (3 + m) * GS)), xi2, fma(__ldg(gcol + (6 + m) * GS), xi3, __ldg(gcol + m * GS)));
+          b2[m] = fma(__ldg(gcol + (18 + m) * GS), xi3, __ldg(gcol + (12 + m) * GS));
+          s2[m] = fma(__ldg(gcol + (21 + m) * GS), xi3, __ldg(gcol + (15 + m) * GS));
+          b3[m] = fma(__ldg(gcol + (30 + m) * GS), xi2, __ldg(gcol + (24 + m) * GS));
+          s3[m] = fma(__ldg(gcol + (33 + m) * GS), xi2, __ldg(gcol + (27 + m) * GS));
+        }
+        const double sq = __ldg(gcol + 36 * GS) * gq[Q + a2] * gq[Q + a3];
 #pragma unroll
-        for (int f = 0; f < 9; ++f) A[f] = __ldg(q + f * 32);
-        pointwise(G[a1], A, r);
+        for (int a1 = 0; a1 < Q; ++a1) {
+          const double xi1 = gq[a1];
+          double J[3][3];
+#pragma unroll
+          for (int m = 0; m < 3; ++m) {
+            J[m][0] = col1[m];
+            J[m][1] = fma(s2[m], xi1, b2[m]);
+            J[m][2] = fma(s3[m], xi1, b3[m]);
+          }
+          double adj[3][3];
+          adj[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+          adj[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+          adj[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+          adj[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+          adj[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+          adj[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+          adj[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+          adj[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+          adj[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+          const double det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
+          const double sc = sq * gq[Q + a1] * rsqrt(det);
+          double A[9];
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+#pragma unroll
+            for (int m = 0; m < 3; ++m) A[3 * d + m] = sc * adj[d][m];
+          pointwise(G[a1], A, r);
+        }
+      } else {
+#pragma unroll
+        for (int a1 = 0; a1 < Q; ++a1) {
+          const double* q = qb + (int64_t)((a1 + Q * (a2 + Q * a3)) * 9) * 32;
+          double A[9];
+#pragma unroll
+          for (int f = 0; f < 9; ++f) A[f] = __ldg(q + f * 32);
+          pointwise(G[a1], A, r);
+        }
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c)
@@ -181,30 +234,33 @@ __global__ void __launch_bounds__(NT, ELAS_P1T_MINB)
       }
 }
 
-template <int Q>
+template <int Q, bool OTF>
 cudaError_t launch_q(const Slab& s, const double* x, double* y, const double* qd, const double* rr,
-                     const double* tables, int64_t e_begin, int64_t e_end, cudaStream_t st) {
+                     const double* tables, int64_t e_begin, int64_t e_end, cudaStream_t st, const double* gauss) {
   static int pref = -1;
   if (pref < 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_p1_kernel<Q>, NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_p1_kernel<Q, OTF>, NT, 0);
     pref = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
   const int64_t grid = (ne + NT - 1) / NT;
-  apply_p1_kernel<Q><<<(unsigned)grid, NT, 0, st>>>(x, y, qd, rr, tables, s, e_begin, e_end, pref);
+  apply_p1_kernel<Q, OTF><<<(unsigned)grid, NT, 0, st>>>(x, y, qd, rr, tables, s, e_begin, e_end, pref, gauss);
   return cudaGetLastError();
 }
 
 }  // namespace lo
 
 cudaError_t apply_p1t_launch(int q, const Slab& s, const double* x, double* y, const double* qd, const double* rr,
-                             const double* tables, int64_t e_begin, int64_t e_end, cudaStream_t st) {
-  if (q == 2) return lo::launch_q<2>(s, x, y, qd, rr, tables, e_begin, e_end, st);
-  if (q == 3) return lo::launch_q<3>(s, x, y, qd, rr, tables, e_begin, e_end, st);
+                             const double* tables, int64_t e_begin, int64_t e_end, cudaStream_t st, int otf) {
+  const double* gauss = tables + tables_gauss_offset(1, q, fold_table_size(1, q));
+  if (q == 2) return otf ? lo::launch_q<2, true>(s, x, y, qd, rr, tables, e_begin, e_end, st, gauss)
+                         : lo::launch_q<2, false>(s, x, y, qd, rr, tables, e_begin, e_end, st, gauss);
+  if (q == 3) return otf ? lo::launch_q<3, true>(s, x, y, qd, rr, tables, e_begin, e_end, st, gauss)
+                         : lo::launch_q<3, false>(s, x, y, qd, rr, tables, e_begin, e_end, st, gauss);
   return cudaErrorInvalidValue;
 }
 

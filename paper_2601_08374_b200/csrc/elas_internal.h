@@ -63,7 +63,10 @@ cudaError_t apply_tc_launch(const Slab& s, const double* x, double* y, const dou
 //     Jacobian coefficients, geo[e][GEO_WORDS]: dx/dxi1 = c0 + c1 xi2 + c2 xi3 + c3 xi2 xi3,
 //     dx/dxi2 = e0 + e1 xi1 + e2 xi3 + e3 xi1 xi3, dx/dxi3 = f0 + f1 xi1 + f2 xi2 + f3 xi1 xi2
 //     (3-vectors: c0..c3 at 0..11, e at 12..23, f at 24..35), sqrt(mu_e) at 36.
-enum { QD_LAYOUT_LINES = 0, QD_LAYOUT_TC6 = 1, QD_LAYOUT_E32 = 2, QD_LAYOUT_LINES_F32 = 3, QD_LAYOUT_OTF = 4 };
+// 5 = layout 4 lane-interleaved over blocks of 32 elements (p = 1 thread-per-element kernel):
+//     geo32[e / 32][w][e % 32].
+enum { QD_LAYOUT_LINES = 0, QD_LAYOUT_TC6 = 1, QD_LAYOUT_E32 = 2, QD_LAYOUT_LINES_F32 = 3, QD_LAYOUT_OTF = 4,
+       QD_LAYOUT_OTF32 = 5 };
 constexpr int GEO_WORDS = 40;
 
 // qdata doubles per element: 9 q^3 rounded up to even so every element starts 16-B aligned
@@ -72,18 +75,21 @@ constexpr int qd_stride_lines(int q) { return (9 * q * q * q + 1) & ~1; }
 inline int qd_stride(int q, int layout) {
   return layout == QD_LAYOUT_LINES       ? qd_stride_lines(q)
          : layout == QD_LAYOUT_LINES_F32 ? (9 * q * q * q + 3) & ~3
-         : layout == QD_LAYOUT_OTF       ? GEO_WORDS
+         : (layout == QD_LAYOUT_OTF || layout == QD_LAYOUT_OTF32) ? GEO_WORDS
                                          : 9 * q * q * q;
 }
 // op tables: B | D | fold(B) | fold(D) | Gauss points g[q] | sqrt(w)[q]
 inline int tables_gauss_offset(int p, int q, int fts) { return 2 * q * (p + 1) + 2 * fts; }
 inline size_t qd_word_bytes(int layout) { return layout == QD_LAYOUT_LINES_F32 ? 4 : 8; }
 // elements the qdata allocation must cover (E32 pads to whole blocks of 32)
-inline int64_t qd_elems(int64_t ne, int layout) { return layout == QD_LAYOUT_E32 ? (ne + 31) / 32 * 32 : ne; }
+inline int64_t qd_elems(int64_t ne, int layout) {
+  return (layout == QD_LAYOUT_E32 || layout == QD_LAYOUT_OTF32) ? (ne + 31) / 32 * 32 : ne;
+}
 
 // one-thread-per-element kernel, p = 1 (elas_apply_p1t.cu)
+// otf = 1: geometry on the fly (qd = geo32, QD_LAYOUT_OTF32; tables must carry the Gauss points)
 cudaError_t apply_p1t_launch(int q, const Slab& s, const double* x, double* y, const double* qd, const double* rr,
-                             const double* tables, int64_t e_begin, int64_t e_end, cudaStream_t st);
+                             const double* tables, int64_t e_begin, int64_t e_end, cudaStream_t st, int otf = 0);
 
 // Kernels in elas_setup.cu
 cudaError_t launch_qdata(int p, int q, int layout, const Slab& s, const double* verts, const double* lam,

@@ -73,7 +73,7 @@ __global__ void qdata_kernel(int q, int layout, Slab s, const double* __restrict
     }
     const double W = qp.w[a1] * qp.w[a2] * qp.w[a3] * det;
     const double sc = sqrt(mu[e] * W) / det;   // A~ = sqrt(mu W) J^{-1} = sqrt(mu W) adj / det
-    if (layout == QD_LAYOUT_OTF) {   // geometry on the fly: the det check above at every point,
+    if (layout == QD_LAYOUT_OTF || layout == QD_LAYOUT_OTF32) {   // geometry on the fly: det check above,
       if (pt == 0) {                   // the Jacobian polynomial coefficients once per element
         double Xv[2][2][2][3];
         for (int c = 0; c < 2; ++c)
@@ -82,7 +82,8 @@ __global__ void qdata_kernel(int q, int layout, Slab s, const double* __restrict
               const int64_t v = ((int64_t)(ez + c) * (s.ny + 1) + (ey + b)) * (s.nx + 1) + (ex + a);
               for (int m = 0; m < 3; ++m) Xv[a][b][c][m] = V[v * 3 + m];
             }
-        double* o = qd + e * (int64_t)GEO_WORDS;
+        double ow[GEO_WORDS];
+        double* o = ow;
         for (int m = 0; m < 3; ++m) {
           // d/dxi1: differences along a, bilinear in (xi2 = b, xi3 = c)
           const double d00 = Xv[1][0][0][m] - Xv[0][0][0][m], d10 = Xv[1][1][0][m] - Xv[0][1][0][m];
@@ -99,6 +100,10 @@ __global__ void qdata_kernel(int q, int layout, Slab s, const double* __restrict
         }
         o[36] = sqrt(mu[e]);
         o[37] = o[38] = o[39] = 0.0;
+        for (int w = 0; w < GEO_WORDS; ++w) {
+          if (layout == QD_LAYOUT_OTF) qd[e * (int64_t)GEO_WORDS + w] = ow[w];
+          else qd[(e >> 5) * (int64_t)(32 * GEO_WORDS) + w * 32 + (e & 31)] = ow[w];
+        }
       }
     } else if (layout == QD_LAYOUT_E32) {
       double* out = qd + (e >> 5) * (int64_t)(32 * 9 * q3) + (int64_t)pt * 9 * 32 + (e & 31);

@@ -81,14 +81,14 @@ __device__ __forceinline__ int64_t qd_offset(int layout, int q, int64_t e, int a
 }
 
 // A~ at point (a1, a2, a3) from the geometry-on-the-fly coefficients (QD_LAYOUT_OTF)
-__device__ __forceinline__ void otf_A(const double* ge, const double* g, const double* sw, int a1, int a2, int a3,
-                                      double (&A)[9]) {
+__device__ __forceinline__ void otf_A(const double* ge, int st, const double* g, const double* sw, int a1, int a2,
+                                      int a3, double (&A)[9]) {
   const double x1 = g[a1], x2 = g[a2], x3 = g[a3];
   double J[3][3];
   for (int m = 0; m < 3; ++m) {
-    J[m][0] = ge[m] + ge[3 + m] * x2 + ge[6 + m] * x3 + ge[9 + m] * x2 * x3;
-    J[m][1] = ge[12 + m] + ge[15 + m] * x1 + ge[18 + m] * x3 + ge[21 + m] * x1 * x3;
-    J[m][2] = ge[24 + m] + ge[27 + m] * x1 + ge[30 + m] * x2 + ge[33 + m] * x1 * x2;
+    J[m][0] = ge[m * st] + ge[(3 + m) * st] * x2 + ge[(6 + m) * st] * x3 + ge[(9 + m) * st] * x2 * x3;
+    J[m][1] = ge[(12 + m) * st] + ge[(15 + m) * st] * x1 + ge[(18 + m) * st] * x3 + ge[(21 + m) * st] * x1 * x3;
+    J[m][2] = ge[(24 + m) * st] + ge[(27 + m) * st] * x1 + ge[(30 + m) * st] * x2 + ge[(33 + m) * st] * x1 * x2;
   }
   double adj[3][3];
   adj[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
@@ -101,7 +101,7 @@ __device__ __forceinline__ void otf_A(const double* ge, const double* g, const d
   adj[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
   adj[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
   const double det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
-  const double sc = ge[36] * sw[a1] * sw[a2] * sw[a3] * rsqrt(det);
+  const double sc = ge[36 * st] * sw[a1] * sw[a2] * sw[a3] * rsqrt(det);
   for (int d = 0; d < 3; ++d)
     for (int m = 0; m < 3; ++m) A[3 * d + m] = sc * adj[d][m];
 }
@@ -144,9 +144,10 @@ __global__ void __launch_bounds__(128) diag_kernel(int p, int q, int layout, Sla
     for (int pt = tid; pt < q3; pt += NT) {
       const int a1 = pt % q, a2 = (pt / q) % q, a3 = pt / (q * q);
       double Ak[3], Al[3];
-      if (layout == QD_LAYOUT_OTF) {
+      if (layout == QD_LAYOUT_OTF || layout == QD_LAYOUT_OTF32) {
         double A[9];
-        otf_A(qd + e * (int64_t)GEO_WORDS, gauss, gauss + q, a1, a2, a3, A);
+        if (layout == QD_LAYOUT_OTF) otf_A(qd + e * (int64_t)GEO_WORDS, 1, gauss, gauss + q, a1, a2, a3, A);
+        else otf_A(qd + (e >> 5) * (int64_t)(32 * GEO_WORDS) + (e & 31), 32, gauss, gauss + q, a1, a2, a3, A);
         for (int m = 0; m < 3; ++m) {
           Ak[m] = A[3 * k + m];
           Al[m] = A[3 * l + m];
