@@ -114,6 +114,9 @@ template <int P> struct StageEO { static constexpr bool value = P != 2 && !(P ==
 #ifndef ELAS_QD_L1PF
 #define ELAS_QD_L1PF 0
 #endif
+#ifndef ELAS_X_PREFETCH
+#define ELAS_X_PREFETCH 0
+#endif
 #ifndef ELAS_QD_RING_ALIAS
 #define ELAS_QD_RING_ALIAS 1
 #endif
@@ -331,6 +334,22 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
       const uintptr_t a1 = a0 + (uintptr_t)(pne * C::QDE * sizeof(T));
       const uintptr_t lo = a0 & ~(uintptr_t)15, hi = (a1 + 15) & ~(uintptr_t)15;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
+    }
+  }
+#endif
+#if ELAS_X_PREFETCH
+  // the z-column this thread will gather in the CTA one wave ahead, pulled into L2 now
+  if (!COLORED && pref_ctas > 0) {
+    const int64_t pe = e0 + (int64_t)pref_ctas * EB + zel;
+    if (zel < EB && tid < EB * N * N && pe < e_end) {
+      int pex, pey, pez;
+      elem_coords<false>(cm, s, pe, pex, pey, pez);
+      const int64_t pbase = (pex * P + zi) + (int64_t)s.Nx * (pey * P + zj) + plane * ((int64_t)pez * P);
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(x + c * s.nodes + pbase + k * plane));
     }
   }
 #endif
