@@ -27,6 +27,9 @@ static constexpr bool kAutoThread = ELAS_AUTO_THREAD != 0;
 #define ELAS_AUTO_FOLDED 1
 #endif
 static constexpr bool kAutoFolded = ELAS_AUTO_FOLDED != 0;
+#ifndef ELAS_HOST_CHUNKS
+#define ELAS_HOST_CHUNKS 64   // z-chunks of the pipelined host apply
+#endif
 
 namespace elas {
 
@@ -634,7 +637,7 @@ int elas_apply_host(elas_op* op, const double* xh, double* yh) {
   // streams (PCIe is full duplex; the apply is ~10x faster than either copy).  Plane K of y is
   // final once every element layer touching it has been applied: after chunk k, planes below
   // its top plane are final.
-  const int nchunk = s.nz < 64 ? s.nz : 64;   // fill + drain cost ~2/nchunk of the copy time
+  const int nchunk = s.nz < ELAS_HOST_CHUNKS ? s.nz : ELAS_HOST_CHUNKS;   // fill + drain ~2/nchunk of the copies
   if (!op->h2d) CUDA_OR(cudaStreamCreateWithFlags(&op->h2d, cudaStreamNonBlocking), "cudaStreamCreate");
   if (!op->d2h) CUDA_OR(cudaStreamCreateWithFlags(&op->d2h, cudaStreamNonBlocking), "cudaStreamCreate");
   while ((int)op->host_ev.size() < 2 * nchunk + 1) {
