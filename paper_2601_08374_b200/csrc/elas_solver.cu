@@ -205,13 +205,15 @@ __global__ void __launch_bounds__(128) diag_kernel(int p, int q, int layout, Sla
 
 // partial[b] = sum over this block's grid-stride share of w_i a_i b_i (w_i = 0 on interface
 // planes owned by the rank below; none for one rank)
-// partial[b] = this block's share of sum_c sum_{node >= skip} a b over the 3 components.  skip =
-// one node plane on ranks > 0 of a slab partition: the lower interface plane is replicated and
-// owned by the rank below, so every dof is counted once in the allreduced dot.
-__global__ void __launch_bounds__(RED_THREADS) dot_partial_kernel(const double* __restrict__ a,
-                                                                  const double* __restrict__ b, int64_t nodes,
-                                                                  int64_t skip, double* __restrict__ partial) {
+// One-launch deterministic dot: every block writes its partial of sum_c sum_{node >= skip} a b
+// (skip = one node plane on ranks > 0 of a slab partition: the lower interface plane is
+// replicated and owned by the rank below), and the LAST block to finish (atomic ticket) sums the
+// RED_BLOCKS partials in a fixed tree order into *out and re-arms the ticket.
+__global__ void __launch_bounds__(RED_THREADS) dot_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                                          int64_t nodes, int64_t skip, double* __restrict__ partial,
+                                                          double* __restrict__ out, unsigned int* __restrict__ ticket) {
   __shared__ double sh[RED_THREADS];
+  __shared__ bool last;
   double v = 0.0;
   for (int c = 0; c < 3; ++c) {
     const double* ac = a + c * nodes;
@@ -226,21 +228,26 @@ __global__ void __launch_bounds__(RED_THREADS) dot_partial_kernel(const double* 
     if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
-}
-
-__global__ void __launch_bounds__(RED_THREADS) dot_final_kernel(const double* __restrict__ partial,
-                                                                double* __restrict__ out) {
-  __shared__ double sh[RED_THREADS];
-  double v = 0.0;
-  for (int b = threadIdx.x; b < RED_BLOCKS; b += RED_THREADS) v += partial[b];
-  sh[threadIdx.x] = v;
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = sh[0];
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
   __syncthreads();
-  for (int w = RED_THREADS / 2; w > 0; w >>= 1) {
-    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+  if (!last) return;
+  __threadfence();
+  double w = 0.0;
+  for (int bb = threadIdx.x; bb < RED_BLOCKS; bb += RED_THREADS) w += ((volatile double*)partial)[bb];
+  sh[threadIdx.x] = w;
+  __syncthreads();
+  for (int k = RED_THREADS / 2; k > 0; k >>= 1) {
+    if ((int)threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = sh[0];
+  if (threadIdx.x == 0) {
+    *out = sh[0];
+    *ticket = 0u;
+  }
 }
 
 // distributed dot over the owned dofs of this rank, result in the device scalar `slot`
@@ -249,8 +256,8 @@ int dot(elas_op* op, const double* a, const double* b, int slot) {
   const Slab& s = op->slab;
   cudaStream_t st = op->stream;
   const int64_t skip = op->rank > 0 ? (int64_t)s.Nx * s.Ny : 0;
-  dot_partial_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, b, s.nodes, skip, op->red);
-  dot_final_kernel<<<1, RED_THREADS, 0, st>>>(op->red, op->red + RED_BLOCKS + slot);
+  dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, b, s.nodes, skip, op->red, op->red + RED_BLOCKS + slot,
+                                                reinterpret_cast<unsigned int*>(op->red + RED_BLOCKS + S_COUNT));
   CK(cudaGetLastError(), "dot kernels");
   if (op->comm) {
     ncclResult_t r = ncclAllReduce(op->red + RED_BLOCKS + slot, op->red + RED_BLOCKS + slot, 1, ncclDouble, ncclSum,
@@ -346,7 +353,10 @@ __global__ void splitmix_kernel(double* __restrict__ v, int64_t n, unsigned long
 }
 
 int ensure_red(elas_op* op) {
-  if (!op->red) CK(cudaMalloc(&op->red, sizeof(double) * (RED_BLOCKS + S_COUNT)), "cudaMalloc (reduction scratch)");
+  if (!op->red) {
+    CK(cudaMalloc(&op->red, sizeof(double) * (RED_BLOCKS + S_COUNT + 1)), "cudaMalloc (reduction scratch)");
+    CK(cudaMemset(op->red, 0, sizeof(double) * (RED_BLOCKS + S_COUNT + 1)), "cudaMemset (reduction scratch)");
+  }
   return ELAS_OK;
 }
 
