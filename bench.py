@@ -248,6 +248,36 @@ def sweep_config4(reps=10, warmup=3, variant=0, ps=range(1, 9)):
 
 # ------------------------------------------------------------------------------ config 2 hot / cold
 
+def small_configs(reps=20):
+    """Config 1 (375 DoF: launch/latency-bound, time only) and config 3 (9.1M DoF,
+    Dirichlet face) per-apply numbers on the AUTO kernel."""
+    import torch
+    import synth
+    from paper_2601_08374_b200.elas import Operator
+    out = {}
+    for cfg in (1, 3):
+        P = synth.make_config(cfg)
+        op = Operator.from_problem(P)
+        x = torch.from_numpy(P.x).cuda()
+        y = torch.empty_like(x)
+        for _ in range(5):
+            op.apply(x, y)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            op.apply(x, y)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        out[f"cfg{cfg}"] = {"dofs": P.num_dofs, "ms_per_apply": round(ms, 5),
+                            "gdofs": round(P.num_dofs / ms / 1e6, 3) if cfg != 1 else None}
+        op.close()
+        del x, y
+        torch.cuda.empty_cache()
+    return out
+
+
 def config2_hot_cold(reps=20):
     """Config 2 (823,875 DoF; 77 MB working set < 126 MB L2): back-to-back applies (hot) and
     applies each preceded by a 2 x L2 memset (cold), per SURVEY 8(d)."""
@@ -553,6 +583,7 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(P)
     if ws == 1 and not args.no_sweep:
         line["config2_hot_cold"] = config2_hot_cold()
+        line["configs_1_3"] = small_configs()
     if ws == 1 and not args.no_solver:
         line["solver"] = solver_bench()
     if ws == 1 and not args.no_sweep:
