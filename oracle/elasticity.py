@@ -27,6 +27,7 @@ vectors are component-blocked: dof = c N + node (local: c n^3 + l).
 """
 
 from dataclasses import dataclass
+from typing import Optional
 
 import numpy as np
 
@@ -45,6 +46,7 @@ class Mesh:
     lam: np.ndarray               # (nz, ny, nx) per-element lambda
     mu: np.ndarray                # (nz, ny, nx) per-element mu
     dirichlet_faces: int = 0
+    C6: Optional[np.ndarray] = None   # anisotropic (Eq. 2): (nz, ny, nx, 6, 6) Voigt matrices; replaces lam, mu
 
     def __post_init__(self):
         self.vertices = np.ascontiguousarray(self.vertices, dtype=np.float64)
@@ -54,6 +56,8 @@ class Mesh:
         shape = (self.nz, self.ny, self.nx)
         self.lam = np.broadcast_to(np.asarray(self.lam, dtype=np.float64), shape)
         self.mu = np.broadcast_to(np.asarray(self.mu, dtype=np.float64), shape)
+        if self.C6 is not None:
+            self.C6 = np.broadcast_to(np.asarray(self.C6, dtype=np.float64), shape + (6, 6))
 
     @property
     def n(self):
@@ -154,6 +158,39 @@ def element_stiffness(X, lam, mu, tables, rows=None):
     return K.reshape(R, 3 * nn)
 
 
+VOIGT = np.array([[0, 5, 4], [5, 1, 3], [4, 3, 2]])   # (i, j) -> Voigt index [11,22,33,23,13,12]
+
+
+def element_stiffness_aniso(X, C6, tables, rows=None):
+    """Element stiffness for a general anisotropic material (Eq. 2):
+    sigma_voigt = C eps_voigt with eps_voigt = [e11, e22, e33, 2e23, 2e13, 2e12],
+    i.e. C_ijkl = C6[v(i,j)][v(k,l)], and
+        K[(i,I),(j,J)] = sum_qp W sum_{k,l} d_k phi_I C_ikjl d_l phi_J .
+    """
+    Gref, w3, g = tables
+    nn = Gref.shape[1]
+    J, detJ, W = element_geometry(X, g, w3)
+    A = np.linalg.inv(J)
+    Phi = np.einsum("klq,qkm->mlq", Gref, A, optimize=True)        # Phi[m][l, qp] = d_m phi_l
+    C4 = C6[VOIGT[:, :, None, None], VOIGT[None, None, :, :]]      # C4[i, k, j, l]
+    if rows is None:
+        rows = np.arange(3 * nn)
+    rows = np.asarray(rows)
+    comp, node = rows // nn, rows % nn
+    PW = Phi[:, node, :] * W                                       # (3, R, q)
+    # K[r, j, J] = sum_{k,l} C4[i_r, k, j, l] sum_q PW[k, r, q] Phi[l, J, q]
+    M = np.einsum("krq,lJq->klrJ", PW, Phi, optimize=True)         # (3, 3, R, n^3)
+    K = np.einsum("rkjl,klrJ->rjJ", C4[comp], M, optimize=True)    # (R, 3, n^3)
+    return K.reshape(rows.size, 3 * nn)
+
+
+def _stiffness(mesh, ex, ey, ez, tables, rows=None):
+    X = element_vertices(mesh, ex, ey, ez)
+    if mesh.C6 is not None:
+        return element_stiffness_aniso(X, mesh.C6[ez, ey, ex], tables, rows)
+    return element_stiffness(X, mesh.lam[ez, ey, ex], mesh.mu[ez, ey, ex], tables, rows)
+
+
 # ----------------------------------------------------------------------------------------
 # Element restriction G (gather) and its transpose (scatter), Dirichlet mask Z
 # ----------------------------------------------------------------------------------------
@@ -209,8 +246,7 @@ def apply_elements(mesh, xz, elements):
     for ex, ey, ez in elements:
         nodes = element_nodes(mesh, ex, ey, ez)
         dofs = np.concatenate([c * N + nodes for c in range(3)])
-        K = element_stiffness(element_vertices(mesh, ex, ey, ez),
-                              mesh.lam[ez, ey, ex], mesh.mu[ez, ey, ex], tables)
+        K = _stiffness(mesh, ex, ey, ez, tables)
         np.add.at(y, dofs, K @ xz[dofs])
     return y
 
@@ -249,8 +285,7 @@ def apply_rows(mesh, x, dofs):
         edofs = np.concatenate([c * N + nodes for c in range(3)])
         pos = np.array([a for a, _ in lst])
         lrows = np.array([b for _, b in lst])
-        K = element_stiffness(element_vertices(mesh, ex, ey, ez),
-                              mesh.lam[ez, ey, ex], mesh.mu[ez, ey, ex], tables, rows=lrows)
+        K = _stiffness(mesh, ex, ey, ez, tables, rows=lrows)
         np.add.at(y, pos, K @ xz[edofs])
     return y
 
@@ -263,8 +298,7 @@ def assemble_dense(mesh):
     for ex, ey, ez in _elements(mesh):
         nodes = element_nodes(mesh, ex, ey, ez)
         dofs = np.concatenate([c * N + nodes for c in range(3)])
-        K = element_stiffness(element_vertices(mesh, ex, ey, ez),
-                              mesh.lam[ez, ey, ex], mesh.mu[ez, ey, ex], tables)
+        K = _stiffness(mesh, ex, ey, ez, tables)
         A[np.ix_(dofs, dofs)] += K
     Z = constrained_mask(mesh)
     A[Z, :] = 0.0

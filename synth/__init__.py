@@ -173,3 +173,19 @@ def splitmix_uniform(n, seed):
         z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
         z = z ^ (z >> np.uint64(31))
     return 2.0 * (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53) - 1.0
+
+
+def isotropic_C6(lam, mu):
+    """The 6x6 Voigt matrix of Hooke's law (Eq. 3) -- an input-construction helper (no operator)."""
+    C = np.zeros((6, 6))
+    C[:3, :3] = lam
+    C[[0, 1, 2], [0, 1, 2]] = lam + 2 * mu
+    C[[3, 4, 5], [3, 4, 5]] = mu
+    return C
+
+
+def random_C6(rng, shape, scale=1.0):
+    """Seeded symmetric positive-definite 6x6 Voigt matrices (general anisotropic materials, Eq. 2):
+    C = L L^T + 0.5 I with L ~ N(0, 0.3^2) entries, times `scale`; shape (..., 6, 6)."""
+    L = rng.normal(0.0, 0.3, size=tuple(shape) + (6, 6))
+    return scale * (L @ np.swapaxes(L, -1, -2) + 0.5 * np.eye(6))
