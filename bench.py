@@ -278,6 +278,34 @@ def small_configs(reps=20):
     return out
 
 
+def anisotropic_sweep(ps=(2, 4, 6, 8), reps=10):
+    """General anisotropic material (Eq. 2): config 4 with a seeded SPD Voigt matrix per element."""
+    import numpy as np
+    import torch
+    import synth
+    from paper_2601_08374_b200.elas import Operator
+    out = {}
+    for p in ps:
+        P = synth.make_config(4, p)
+        x = torch.from_numpy(P.x).cuda()
+        y = torch.empty_like(x)
+        op = Operator.anisotropic(P, synth.random_C6(np.random.default_rng(p), (P.nz, P.ny, P.nx)))
+        for _ in range(3):
+            op.apply(x, y)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            op.apply(x, y)
+        b.record()
+        torch.cuda.synchronize()
+        out[str(p)] = round(P.num_dofs / (a.elapsed_time(b) / reps / 1e3) / 1e9, 3)
+        op.close()
+        del x, y
+        torch.cuda.empty_cache()
+    return {"workload": "config 4, C_e = L L^T + 0.5 I per element (seeded), folded FP64 kernel", "gdofs": out}
+
+
 def config2_hot_cold(reps=20):
     """Config 2 (823,875 DoF; 77 MB working set < 126 MB L2): back-to-back applies (hot) and
     applies each preceded by a 2 x L2 memset (cold), per SURVEY 8(d)."""
@@ -584,6 +612,7 @@ def run_ours(args):
     if ws == 1 and not args.no_sweep:
         line["config2_hot_cold"] = config2_hot_cold()
         line["configs_1_3"] = small_configs()
+        line["anisotropic"] = anisotropic_sweep()
     if ws == 1 and not args.no_solver:
         line["solver"] = solver_bench()
     if ws == 1 and not args.no_sweep:

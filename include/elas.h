@@ -83,6 +83,15 @@ typedef struct {
  * Returns NULL on error (see elas_last_error). */
 elas_op* elas_create(const elas_mesh* mesh, int p, int q, const double* lambda, const double* mu);
 
+/* General anisotropic material (Eq. 2): sigma_voigt = C eps_voigt with
+ * eps_voigt = [e11, e22, e33, 2 e23, 2 e13, 2 e12].  C21: HOST, the upper
+ * triangle of the symmetric 6 x 6 Voigt matrix row by row (C00 C01 .. C05 C11 .. C55), 21
+ * doubles per element (mesh->material_per_element = 1, element order as lambda/mu) or 21 for
+ * all.  The op runs the folded FP64 kernel with A~ = sqrt(W) J^{-1} and a 6 x 6 product per
+ * point; elas_apply, elas_diagonal, Chebyshev, PCG and the deterministic mode work unchanged.
+ * NULL + message on error (as elas_create; non-finite entries are ELAS_EINVAL). */
+elas_op* elas_create_aniso(const elas_mesh* mesh, int p, int q, const double* C21);
+
 /* Kernel variants of the fused apply (same operator, same results to rounding):
  *   ELAS_VARIANT_SIMT   FP64 FMA pipe, one thread per 1D fibre (every p, q);
  *   ELAS_VARIANT_TENSOR FP64 tensor cores (mma.sync f64 / DMMA), one warp per element

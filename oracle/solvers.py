@@ -51,9 +51,17 @@ def diagonal(mesh):
         J, detJ, W = element_geometry(element_vertices(mesh, ex, ey, ez), g, w3)
         A = np.linalg.inv(J)
         Phi = np.einsum("klq,qkm->mlq", Gref, A)            # Phi[m][l, qp] = d_m phi_l
+        nodes = element_nodes(mesh, ex, ey, ez)
+        if mesh.C6 is not None:   # Eq. 2: sum_qp W sum_kl d_k phi C_ckcl d_l phi
+            from .elasticity import VOIGT
+            C6 = mesh.C6[ez, ey, ex]
+            PP = np.einsum("kiq,liq,q->kli", Phi, Phi, W)               # (3, 3, n^3)
+            for c in range(3):
+                Cc = C6[VOIGT[c][:, None], VOIGT[c][None, :]]           # Cc[k, l] = C_ckcl
+                np.add.at(d, c * N + nodes, np.einsum("kl,kli->i", Cc, PP))
+            continue
         lam, mu = mesh.lam[ez, ey, ex], mesh.mu[ez, ey, ex]
         sq = np.einsum("mlq,q->ml", Phi ** 2, W)             # sum_qp W (d_m phi_l)^2
-        nodes = element_nodes(mesh, ex, ey, ez)
         tot = sq.sum(axis=0)
         for c in range(3):
             np.add.at(d, c * N + nodes, (lam + mu) * sq[c] + mu * tot)

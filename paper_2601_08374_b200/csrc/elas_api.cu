@@ -51,7 +51,7 @@ DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
   cudaError_t apply_eo_launch_p##P(int q, int fp32, const Slab& s, const double* x, double* y,   \
                                    const void* qd, const double* rr, const void* tables,        \
                                    int64_t e_begin, int64_t e_end, cudaStream_t st, const int* color, \
-                                   int otf);
+                                   int otf, const double* cc);
 DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
 #undef DECL
 
@@ -93,9 +93,9 @@ cudaError_t apply_eo_info(int p, int q, int fp32, ApplyLaunch* info) {
 
 cudaError_t apply_eo_launch(int p, int q, int fp32, const Slab& s, const double* x, double* y, const void* qd,
                             const double* rr, const void* tables, int64_t e_begin, int64_t e_end,
-                            cudaStream_t st, const int* color, int otf) {
+                            cudaStream_t st, const int* color, int otf, const double* cc) {
   switch (p) {
-#define CASE(P) case P: return apply_eo_launch_p##P(q, fp32, s, x, y, qd, rr, tables, e_begin, e_end, st, color, otf);
+#define CASE(P) case P: return apply_eo_launch_p##P(q, fp32, s, x, y, qd, rr, tables, e_begin, e_end, st, color, otf, cc);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
     default: return cudaErrorInvalidValue;
@@ -138,6 +138,7 @@ void free_op(elas_op* op) {
   cudaFree(op->rr);
   cudaFree(op->tab);
   cudaFree(op->tabf);
+  cudaFree(op->cc);
   cudaFree(op->xs);
   cudaFree(op->ys);
   cudaFree(op->halo_lo);
@@ -308,7 +309,7 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
       const int cm[6] = {cx, cy, cz, ncx, ncy, iz0};
       e = elas::apply_eo_launch(op->p, op->q, op->variant == ELAS_VARIANT_FOLDED_F32, s, x, y, op->qd, op->rr,
                                 op->variant == ELAS_VARIANT_FOLDED_F32 ? (const void*)op->tabf : (const void*)op->tab,
-                                0, cnt, st, cm, op->variant == ELAS_VARIANT_FOLDED_OTF);
+                                0, cnt, st, cm, op->variant == ELAS_VARIANT_FOLDED_OTF, op->cc);
     }
   } else
   e = op->variant == ELAS_VARIANT_TENSOR
@@ -316,7 +317,8 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
                   : op->variant == ELAS_VARIANT_THREAD
                       ? elas::apply_p1t_launch(op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
                   : op->variant == ELAS_VARIANT_FOLDED
-                      ? elas::apply_eo_launch(op->p, op->q, 0, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
+                      ? elas::apply_eo_launch(op->p, op->q, 0, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st,
+                                              nullptr, 0, op->cc)
                   : op->variant == ELAS_VARIANT_FOLDED_F32
                       ? elas::apply_eo_launch(op->p, op->q, 1, op->slab, x, y, op->qd, op->rr, op->tabf, e0, e1, st)
                   : (op->variant == ELAS_VARIANT_FOLDED_OTF && op->p == 1)   // thread-per-element kernel
@@ -473,6 +475,29 @@ elas_op* elas_create_ex(const elas_mesh* m, int p, int q, const double* lambda, 
       op->external = true;
     }
   }
+  return op;
+}
+
+elas_op* elas_create_aniso(const elas_mesh* m, int p, int q, const double* C21) {
+  elas::g_err.clear();
+  if (!m || !C21) { set_error("elas_create_aniso: NULL mesh/C"); return nullptr; }
+  const int64_t nc = 21 * (m->material_per_element ? (int64_t)m->nx * m->ny * m->nz : 1);
+  for (int64_t i = 0; i < nc; ++i)
+    if (!std::isfinite(C21[i])) { set_error("elas_create_aniso: non-finite Voigt matrix entry"); return nullptr; }
+  // quadrature data A~ = sqrt(W) J^{-1}: the isotropic setup with mu = 1, lambda = 0 (r = 0)
+  elas_mesh m1 = *m;
+  m1.material_per_element = 0;
+  const double lam0 = 0.0, mu1 = 1.0;
+  elas_op* op = elas_create_ex(&m1, p, q, &lam0, &mu1, ELAS_VARIANT_FOLDED);
+  if (!op) return nullptr;
+  const int64_t ne = (int64_t)op->slab.nx * op->slab.ny * op->slab.nz;
+  const int64_t off = (int64_t)op->ez0 * m->nx * m->ny;
+  std::vector<double> cch((size_t)ne * 21);
+  for (int64_t e = 0; e < ne; ++e)
+    for (int w = 0; w < 21; ++w) cch[(size_t)e * 21 + w] = m->material_per_element ? C21[(off + e) * 21 + w] : C21[w];
+  cudaError_t ce = cudaMalloc(&op->cc, sizeof(double) * cch.size());
+  if (!ce) ce = cudaMemcpy(op->cc, cch.data(), sizeof(double) * cch.size(), cudaMemcpyHostToDevice);
+  if (ce) { cuda_fail(ce, "cudaMalloc/cudaMemcpy (Voigt matrices)"); free_op(op); return nullptr; }
   return op;
 }
 

@@ -223,11 +223,56 @@ struct OtfSmem {
   static constexpr size_t smem = sizeof(T) * (size_t)(OFFG + 2 * Q + C::EB * GEO_WORDS);
 };
 
-template <int P, int Q, typename T, bool COLORED, bool OTF = false>
+// ANISO (general anisotropic material, Eq. 2): the stored qdata is
+// A~ = sqrt(W) J^{-1} (mu = 1, r = 0 at setup) and every element carries its 6 x 6 Voigt matrix
+// (21 upper-triangle words, staged per batch in shared memory).  At a point: H = G A~ =
+// sqrt(W) grad u, eps_v = [H11, H22, H33, H23 + H32, H13 + H31, H12 + H21] (engineering shear,
+// PAPER.md:162), sigma_v = C eps_v, F = sigma~ A~^T = W sigma J^{-T}.
+constexpr int C21 = 21;
+template <int P, int Q, typename T>
+struct AnisoSmem {
+  using C = CfgEO<P, Q, T>;
+  using RG = RingEO<P, Q, T>;
+  static constexpr int OFFC = RG::STAGE ? ((C::BASE + C::EB * C::QDE + 2 + 1) & ~1)
+                                        : ((C::TAB + C::EB * (C::ZE + C::YE) + 1) & ~1);
+  static constexpr size_t smem = sizeof(T) * (size_t)(OFFC + C::EB * C21);
+};
+
+// upper-triangle index of the symmetric 6 x 6 Voigt matrix, row-major: (a, b), a <= b
+__host__ __device__ constexpr int c21_index(int a, int b) {
+  return a <= b ? a * 6 - a * (a - 1) / 2 + (b - a) : b * 6 - b * (b - 1) / 2 + (a - b);
+}
+
+template <typename T>
+__device__ __forceinline__ void pointwise_aniso(T (&g)[3][3], const T (&A)[9], const T* __restrict__ Cs) {
+  T H[3][3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int m = 0; m < 3; ++m) H[c][m] = fma(g[c][2], A[6 + m], fma(g[c][1], A[3 + m], g[c][0] * A[m]));
+  const T ev[6] = {H[0][0], H[1][1], H[2][2], H[1][2] + H[2][1], H[0][2] + H[2][0], H[0][1] + H[1][0]};
+  T sv[6];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    T acc = 0;
+#pragma unroll
+    for (int b = 0; b < 6; ++b) acc = fma(Cs[c21_index(a, b)], ev[b], acc);
+    sv[a] = acc;
+  }
+  const T S[3][3] = {{sv[0], sv[5], sv[4]}, {sv[5], sv[1], sv[3]}, {sv[4], sv[3], sv[2]}};
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      g[c][d] = fma(S[c][2], A[3 * d + 2], fma(S[c][1], A[3 * d + 1], S[c][0] * A[3 * d]));
+}
+
+template <int P, int Q, typename T, bool COLORED, bool OTF = false, bool ANISO = false>
 __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<P>::value : MinbEO<P>::value)
     apply_eo_kernel(const double* __restrict__ x, double* __restrict__ y, const T* __restrict__ qd,
                     const double* __restrict__ rr, const T* __restrict__ tables, Slab s,
-                    int64_t e_begin, int64_t e_end, int pref_ctas, ColorMap cm) {
+                    int64_t e_begin, int64_t e_end, int pref_ctas, ColorMap cm,
+                    const double* __restrict__ cc) {
   using C = CfgEO<P, Q, T>;
   using F = Fold<P, Q>;
   constexpr int N = C::N, NT = C::NT, EB = C::EB;
@@ -312,6 +357,13 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   {
     const T* ft = tables + 2 * Q * N;   // fold(B) | fold(D) follow the plain tables
     for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = ft[t];
+  }
+  if constexpr (ANISO) {   // the batch's Voigt matrices
+    T* cs = smem + AnisoSmem<P, Q, T>::OFFC;
+    for (int t = tid; t < ne * C21; t += NT) {
+      int cex, cey, cez;
+      cs[t] = (T)cc[elem_coords<COLORED>(cm, s, e0 + t / C21, cex, cey, cez) * C21 + t % C21];
+    }
   }
   if constexpr (OTF) {   // Gauss points, sqrt weights and the batch's Jacobian coefficients
     T* gs = smem + OtfSmem<P, Q, T>::OFFG;
@@ -602,7 +654,8 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int d = 0; d < 3; ++d) G[c][d] = g[c][d][a1];
-      pointwise_t<T>(G, A, r);
+      if constexpr (ANISO) pointwise_aniso<T>(G, A, smem + AnisoSmem<P, Q, T>::OFFC + el * C21);
+      else pointwise_t<T>(G, A, r);
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -796,38 +849,41 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   }
 }
 
-template <int P, int Q, typename T, bool COLORED, bool OTF = false>
+template <int P, int Q, typename T, bool COLORED, bool OTF = false, bool ANISO = false>
 cudaError_t launch_apply_eo_pqc(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
                                 const void* tables, int64_t e_begin, int64_t e_end, cudaStream_t st,
-                                const ColorMap& cm) {
+                                const ColorMap& cm, const double* cc = nullptr) {
   using C = CfgEO<P, Q, T>;
-  constexpr size_t SMEM = OTF ? OtfSmem<P, Q, T>::smem : RingEO<P, Q, T>::smem;
+  constexpr size_t SMEM = OTF ? OtfSmem<P, Q, T>::smem : ANISO ? AnisoSmem<P, Q, T>::smem : RingEO<P, Q, T>::smem;
   static bool attr_done = false;
   static int pref = -1;
   if (!attr_done) {
-    cudaError_t err = cudaFuncSetAttribute(apply_eo_kernel<P, Q, T, COLORED, OTF>,
+    cudaError_t err = cudaFuncSetAttribute(apply_eo_kernel<P, Q, T, COLORED, OTF, ANISO>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     if (err != cudaSuccess) return err;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_eo_kernel<P, Q, T, COLORED, OTF>, C::NT, SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_eo_kernel<P, Q, T, COLORED, OTF, ANISO>, C::NT, SMEM);
     pref = sms * (per_sm > 0 ? per_sm : 1);
     attr_done = true;
   }
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
   const int64_t grid = (ne + C::EB - 1) / C::EB;
-  apply_eo_kernel<P, Q, T, COLORED, OTF><<<(unsigned)grid, C::NT, SMEM, st>>>(
-      x, y, static_cast<const T*>(qd), rr, static_cast<const T*>(tables), s, e_begin, e_end, pref, cm);
+  apply_eo_kernel<P, Q, T, COLORED, OTF, ANISO><<<(unsigned)grid, C::NT, SMEM, st>>>(
+      x, y, static_cast<const T*>(qd), rr, static_cast<const T*>(tables), s, e_begin, e_end, pref, cm, cc);
   return cudaGetLastError();
 }
 
 template <int P, int Q, typename T>
 cudaError_t launch_apply_eo_pq(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
                                const void* tables, int64_t e_begin, int64_t e_end, cudaStream_t st,
-                               const ColorMap& cm, int otf) {
+                               const ColorMap& cm, int otf, const double* cc) {
   if constexpr (sizeof(T) == 8) {
+    if (cc)
+      return cm.on ? launch_apply_eo_pqc<P, Q, T, true, false, true>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, cc)
+                   : launch_apply_eo_pqc<P, Q, T, false, false, true>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, cc);
     if (otf)
       return cm.on ? launch_apply_eo_pqc<P, Q, T, true, true>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm)
                    : launch_apply_eo_pqc<P, Q, T, false, true>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm);
@@ -857,15 +913,15 @@ void info_eo_pq(ApplyLaunch* info) {
   cudaError_t apply_eo_launch_p##P(int q, int fp32, const Slab& s, const double* x, double* y,  \
                                    const void* qd, const double* rr, const void* tables,        \
                                    int64_t e_begin, int64_t e_end, cudaStream_t st,             \
-                                   const int* color, int otf) {                                 \
+                                   const int* color, int otf, const double* cc) {               \
     ColorMap cm{0, 0, 0, 0, 0, 0, 0};                                                           \
     if (color) cm = ColorMap{1, color[0], color[1], color[2], color[3], color[4], color[5]};    \
     if (q == P + 1)                                                                             \
-      return fp32 ? launch_apply_eo_pq<P, P + 1, float>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, 0) \
-                  : launch_apply_eo_pq<P, P + 1, double>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, otf); \
+      return fp32 ? launch_apply_eo_pq<P, P + 1, float>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, 0, nullptr) \
+                  : launch_apply_eo_pq<P, P + 1, double>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, otf, cc); \
     if (q == P + 2)                                                                             \
-      return fp32 ? launch_apply_eo_pq<P, P + 2, float>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, 0) \
-                  : launch_apply_eo_pq<P, P + 2, double>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, otf); \
+      return fp32 ? launch_apply_eo_pq<P, P + 2, float>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, 0, nullptr) \
+                  : launch_apply_eo_pq<P, P + 2, double>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, otf, cc); \
     return cudaErrorInvalidValue;                                                               \
   }                                                                                             \
   }

@@ -38,9 +38,10 @@ cudaError_t apply_eo_info(int p, int q, int fp32, ApplyLaunch* info);
 // color == nullptr: elements [e_begin, e_end) with atomic scatter.  color = {cx, cy, cz, ncx, ncy,
 // iz0}: the linear range [e_begin, e_end) of one color's element lattice, plain-RMW scatter.
 // otf = 1: geometry on the fly (FP64 only; qd = geo[e][GEO_WORDS], QD_LAYOUT_OTF)
+// cc != nullptr: anisotropic material (21 Voigt words per element; FP64 only)
 cudaError_t apply_eo_launch(int p, int q, int fp32, const Slab& s, const double* x, double* y, const void* qd,
                             const double* rr, const void* tables, int64_t e_begin, int64_t e_end,
-                            cudaStream_t st, const int* color = nullptr, int otf = 0);
+                            cudaStream_t st, const int* color = nullptr, int otf = 0, const double* cc = nullptr);
 
 // Per-degree translation units (elas_apply_p<P>.cu) export these; q must be p+1 or p+2.
 // Returns cudaSuccess or an error; `info` only queries the configuration.

@@ -17,6 +17,7 @@ struct elas_op {
   bool external = false;            // nranks > 1 without a communicator
   double* qd = nullptr;             // 9 q^3 doubles per element
   double* rr = nullptr;             // lambda/mu per element
+  double* cc = nullptr;             // anisotropic ops: 21 Voigt words per element (elas_create_aniso)
   double* tab = nullptr;            // B | D | fold(B) | fold(D)
   float* tabf = nullptr;            // FP32 copy of tab (mixed-precision folded kernel)
   double* xs = nullptr;             // staging for elas_apply_host

@@ -115,7 +115,8 @@ __global__ void diag_init_kernel(Slab s, double* __restrict__ d) {
 // dynamic smem: B, D (q n each), F[3] (q n each), T0[3][q^3], T1[3][q^2 n], T2[3][q n^2], acc[3][n^3]
 __global__ void __launch_bounds__(128) diag_kernel(int p, int q, int layout, Slab s, const double* __restrict__ qd,
                                                    const double* __restrict__ rr, const double* __restrict__ tables,
-                                                   const double* __restrict__ gauss, double* __restrict__ d) {
+                                                   const double* __restrict__ gauss, const double* __restrict__ cc,
+                                                   double* __restrict__ d) {
   extern __shared__ double sm[];
   const int n = p + 1, qn = q * n, q3 = q * q * q, n3 = n * n * n;
   double* sB = sm;
@@ -163,8 +164,23 @@ __global__ void __launch_bounds__(128) diag_kernel(int p, int q, int layout, Sla
           Al[m] = f32 ? (double)qf[il] : qd[il];
         }
       }
-      const double dot = Ak[0] * Al[0] + Ak[1] * Al[1] + Ak[2] * Al[2];
-      for (int c = 0; c < 3; ++c) T0[c * q3 + pt] = r1 * Ak[c] * Al[c] + dot;
+      if (cc) {   // anisotropic (Eq. 2): M_c,kl = sum_mn A~_km A~_ln C_cmcn, C from 21 Voigt words
+        const double* C = cc + e * 21;
+        const int V[3][3] = {{0, 5, 4}, {5, 1, 3}, {4, 3, 2}};
+        for (int c = 0; c < 3; ++c) {
+          double v = 0.0;
+          for (int m = 0; m < 3; ++m)
+            for (int n2 = 0; n2 < 3; ++n2) {
+              const int a = V[c][m], b = V[c][n2];
+              const int ia = a <= b ? a * 6 - a * (a - 1) / 2 + (b - a) : b * 6 - b * (b - 1) / 2 + (a - b);
+              v = fma(Ak[m] * Al[n2], C[ia], v);
+            }
+          T0[c * q3 + pt] = v;
+        }
+      } else {
+        const double dot = Ak[0] * Al[0] + Ak[1] * Al[1] + Ak[2] * Al[2];
+        for (int c = 0; c < 3; ++c) T0[c * q3 + pt] = r1 * Ak[c] * Al[c] + dot;
+      }
     }
     __syncthreads();
     for (int t = tid; t < 3 * q * q * n; t += NT) {   // x: a1 -> i
@@ -396,7 +412,7 @@ int diag_raw(elas_op* op, double* d) {
   diag_init_kernel<<<grid_for(3 * s.nodes), 256, 0, op->stream>>>(s, d);
   const int64_t ne = (int64_t)s.nx * s.ny * s.nz;
   const double* gauss = op->tab + tables_gauss_offset(p, q, fold_table_size(p, q));
-  if (ne > 0) diag_kernel<<<(unsigned)ne, 128, smem, op->stream>>>(p, q, op->qlayout, s, op->qd, op->rr, op->tab, gauss, d);
+  if (ne > 0) diag_kernel<<<(unsigned)ne, 128, smem, op->stream>>>(p, q, op->qlayout, s, op->qd, op->rr, op->tab, gauss, op->cc, d);
   CK(cudaGetLastError(), "diagonal kernels");
   return exchange_planes(op, d);
 }

@@ -30,7 +30,7 @@ EXPORTED = ["elas_create", "elas_apply", "elas_apply_host", "elas_interface_add"
             "elas_diagonal", "elas_cheb_create", "elas_cheb_lambda_max", "elas_cheb_apply",
             "elas_cheb_destroy", "elas_pcg", "elas_gmg_create", "elas_gmg_level_op", "elas_gmg_levels",
             "elas_gmg_set_stream", "elas_gmg_apply", "elas_pcg_gmg", "elas_gmg_destroy", "elas_gmg_transfer",
-            "elas_set_deterministic", "elas_dot"]
+            "elas_set_deterministic", "elas_dot", "elas_create_aniso"]
 PC_NONE, PC_JACOBI, PC_CHEBYSHEV = 0, 1, 2
 
 
@@ -129,6 +129,8 @@ def load(path=None):
     lib.elas_gmg_apply.argtypes = [P, P, P]
     lib.elas_pcg_gmg.restype = ctypes.c_int
     lib.elas_pcg_gmg.argtypes = [P, P, P, P, ctypes.c_double, ctypes.c_int, ctypes.POINTER(elas_solve_report), D]
+    lib.elas_create_aniso.restype = P
+    lib.elas_create_aniso.argtypes = [ctypes.POINTER(elas_mesh), ctypes.c_int, ctypes.c_int, D]
     lib.elas_dot.restype = ctypes.c_int
     lib.elas_dot.argtypes = [P, P, P, D]
     lib.elas_set_deterministic.restype = ctypes.c_int
@@ -294,6 +296,25 @@ def elas_launches_per_apply(h):
     return load().elas_launches_per_apply(h)
 
 
+def voigt_c21(C6):
+    """Upper triangles (row by row) of symmetric 6 x 6 Voigt matrices: (..., 6, 6) -> (..., 21)."""
+    C6 = np.asarray(C6, dtype=np.float64)
+    iu = np.triu_indices(6)
+    return np.ascontiguousarray(C6[..., iu[0], iu[1]])
+
+
+def elas_create_aniso(nx, ny, nz, p, q, C6, vertices=None, lengths=(1.0, 1.0, 1.0), faces=0):
+    """Anisotropic operator; C6: (6, 6) for all elements or (nz, ny, nx, 6, 6) per element."""
+    C21 = voigt_c21(C6)
+    per = int(C21.ndim > 1)
+    m, lam_a, mu_a, keep = _mesh_args(nx, ny, nz, 1.0, 1.0, vertices, lengths, faces, 0, 1, None)
+    m.material_per_element = per
+    h = load().elas_create_aniso(ctypes.byref(m), p, q, _dptr(C21.reshape(-1)))
+    if not h:
+        raise ElasError(ELAS_EINVAL, f"elas_create_aniso: {elas_last_error()}")
+    return h
+
+
 def elas_dot(h, a, b):
     out = ctypes.c_double(0.0)
     _check(load().elas_dot(h, _ptr(a), _ptr(b), ctypes.byref(out)), "elas_dot")
@@ -399,6 +420,22 @@ class Operator:
         self.local_dofs = elas_local_dofs(self.h)
         self.zrange = elas_local_zrange(self.h)
         self._chebs = []
+
+    @classmethod
+    def anisotropic(cls, P, C6, stream=None):
+        """Operator of the general anisotropic material (Eq. 2) on the mesh of synth.Problem P."""
+        self = cls.__new__(cls)
+        self.p, self.q = P.p, P.q
+        self.h = elas_create_aniso(P.nx, P.ny, P.nz, P.p, P.q, C6, P.vertices, (P.lx, P.ly, P.lz), P.dirichlet_faces)
+        self.variant = elas_variant(self.h)
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream()
+        elas_set_stream(self.h, stream)
+        self.local_dofs = elas_local_dofs(self.h)
+        self.zrange = elas_local_zrange(self.h)
+        self._chebs = []
+        return self
 
     @classmethod
     def from_problem(cls, P, rank=0, nranks=1, nccl_id=None, stream=None, variant=VARIANT_AUTO):

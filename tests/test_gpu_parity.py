@@ -573,3 +573,40 @@ def test_launches_per_apply_matches_profiler():
                    and "Memset" not in e.name and "memset" not in e.name]
         assert len(kernels) == op.launches_per_apply, (faces, det, [k.name for k in kernels])
         op.close()
+
+
+# ---------------------------------------------------------------------------------------
+# general anisotropic material (Eq. 2)
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("p", range(1, 9))
+def test_anisotropic_vs_oracle(p):
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_problem("t", 3, 2, 2, p, p + 2, perturb=True, faces=1 | 32, seed=600 + p)
+    C6 = synth.random_C6(np.random.default_rng(p), (P.nz, P.ny, P.nx))
+    lam, mu = P.material_arrays()
+    m = oracle.Mesh(P.vertex_array(), P.p, P.q, lam, mu, P.dirichlet_faces, C6=C6)
+    op = Operator.anisotropic(P, C6)
+    y = gpu_apply(P, op=op)
+    d = torch.empty(P.num_dofs, dtype=torch.float64, device="cuda")
+    op.diagonal(d)
+    op.set_deterministic(True)
+    y2 = gpu_apply(P, op=op)
+    op.close()
+    assert rel_l2(y, oracle.apply(m, P.x)) <= TOL
+    assert rel_l2(y2, y) <= 1e-14
+    d_ref = oracle.diagonal(m)
+    assert np.abs(d.cpu().numpy() - d_ref).max() <= 1e-12 * np.abs(d_ref).max()
+
+
+def test_anisotropic_isotropic_voigt_equals_isotropic_op():
+    """A single isotropic Voigt matrix through elas_create_aniso == the isotropic operator."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_problem("t", 4, 3, 5, 4, 6, perturb=True, lam=1.3, mu=0.7, faces=1, seed=61)
+    op_i = Operator.from_problem(P)
+    op_a = Operator.anisotropic(P, synth.isotropic_C6(1.3, 0.7))
+    yi, ya = gpu_apply(P, op=op_i), gpu_apply(P, op=op_a)
+    op_i.close(); op_a.close()
+    assert rel_l2(ya, yi) <= 1e-13

@@ -92,3 +92,12 @@ def test_patch_energy(p):
                 vols[k, j, i] = W.sum()
     expect = sum(vols[k, j, i] * ev @ C6[k, j, i] @ ev for k in range(2) for j in range(2) for i in range(2))
     assert abs(u @ A @ u - expect) <= 1e-12 * abs(expect)
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_aniso_diagonal_equals_assembled(p):
+    P = synth.make_problem("t", 2, 2, 2, p, p + 2, perturb=True, faces=1, seed=40 + p)
+    m = aniso_mesh(P, synth.random_C6(np.random.default_rng(7), (2, 2, 2)))
+    d = oracle.diagonal(m)
+    A = oracle.assemble_dense(m)
+    assert np.abs(d - np.diag(A)).max() <= 1e-13 * np.abs(d).max()
