@@ -91,6 +91,14 @@ template <int P> struct MinbEO32 {
   static constexpr int value = P == 7 ? 4 : P == 8 ? 3 : P == 5 ? 2 : (ELAS_EO32_MINB_LO > 0 ? ELAS_EO32_MINB_LO : MinbEO<P>::value);
 };
 
+// Persistent CTAs (measured, config 4): a win only where ONE CTA fills an SM (p = 5: 256 threads,
+// 167 KB smem) and nothing else covers a CTA's start-up latency: 28.4 -> 30.1 GDoF/s; elsewhere
+// the second resident CTA already does and the loop costs registers (p6 33.4 -> 32.3).
+#ifndef ELAS_EO_PERSIST
+#define ELAS_EO_PERSIST 0
+#endif
+template <int P> struct PersistEO { static constexpr bool value = ELAS_EO_PERSIST != 0 || P == 5; };
+
 template <int P, int Q, typename T = double>
 using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEO<P>::value, (int)sizeof(T)>;
 
@@ -290,14 +298,57 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + C::BASE + EB * C::QDE);
 
   const int tid = threadIdx.x;
-  const int64_t e0 = e_begin + (int64_t)blockIdx.x * EB;
+  // PST (persistent CTAs, ELAS_EO_PERSIST): the grid covers the resident CTAs and each walks the
+  // batches b, b + gridDim.x, ...; the next batch's z-columns are gathered into registers right
+  // after the stage-Yt barrier so the loads fly during stage Zt, and the tables load once.
+  constexpr bool PST = PersistEO<P>::value && !COLORED && !OTF && !ANISO;
+  static_assert(EB * N * N <= NT, "stage Z assumes at most one z-column per thread");
+  const int64_t plane = (int64_t)s.Nx * s.Ny;
+  const bool bc = s.faces != 0;
+  const int zi = tid % N, zj = (tid / N) % N, zel = tid / (N * N);
+  const int64_t nbatch = (e_end - e_begin + EB - 1) / EB;
+  const int64_t bstride = PST ? (int64_t)gridDim.x : nbatch;
+  // Stage-Z gather issued before the table copy and the first barrier so that both global
+  // latencies overlap (EB n^2 <= NT: at most one z-column per thread).  Element coordinates in
+  // 32-bit arithmetic (element ids < 2^31).
+  T u[3][N];
+  auto gather = [&](int64_t batch) {
+    const int64_t g0 = e_begin + batch * EB;
+    const int gne = (int)((e_end - g0) < EB ? (e_end - g0) : EB);
+    if (tid < gne * N * N) {
+      int ex, ey, ez;
+      elem_coords<COLORED>(cm, s, g0 + zel, ex, ey, ez);
+      const int I = ex * P + zi, J = ey * P + zj;
+      const int64_t base = I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const bool cons = bc && is_constrained(I, J, ez * P + k, s);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) u[c][k] = cons ? T(0) : (T)__ldg(x + c * s.nodes + base + k * plane);
+      }
+    }
+  };
+  gather(blockIdx.x);
+  {
+    const T* ft = tables + 2 * Q * N;   // fold(B) | fold(D) follow the plain tables
+    for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = ft[t];
+  }
+  if constexpr (STG) {
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
+  uint32_t phase = 0;
+
+  for (int64_t batch = blockIdx.x; batch < nbatch; batch += bstride, phase ^= 1u) {
+  const int64_t e0 = e_begin + batch * EB;
   const int ne = (int)((e_end - e0) < EB ? (e_end - e0) : EB);
+  if constexpr (PST) __syncthreads();   // the previous batch is done with the Z tile and sQ
   if constexpr (STG) {
     if (tid == 0) {
       const uint32_t bar = smem_u32(mbar);
       const uint32_t bytes = (uint32_t)(sizeof(T) * ne * C::QDE);
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
       if constexpr (!COLORED) {
         asm volatile(
@@ -333,31 +384,6 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
 #pragma unroll
     for (int a1 = 0; a1 < R - 1; ++a1) ring_issue(a1);
   }
-  // Stage-Z gather issued before the table copy and the first barrier so that both global
-  // latencies overlap (EB n^2 <= NT: at most one z-column per thread).  Element coordinates in
-  // 32-bit arithmetic (element ids < 2^31).
-  static_assert(EB * N * N <= NT, "stage Z assumes at most one z-column per thread");
-  const int64_t plane = (int64_t)s.Nx * s.Ny;
-  const bool bc = s.faces != 0;
-  const bool zcol = tid < ne * N * N;
-  const int zi = tid % N, zj = (tid / N) % N, zel = tid / (N * N);
-  T u[3][N];
-  if (zcol) {
-    int ex, ey, ez;
-    elem_coords<COLORED>(cm, s, e0 + zel, ex, ey, ez);
-    const int I = ex * P + zi, J = ey * P + zj;
-    const int64_t base = I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      const bool cons = bc && is_constrained(I, J, ez * P + k, s);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) u[c][k] = cons ? T(0) : (T)__ldg(x + c * s.nodes + base + k * plane);
-    }
-  }
-  {
-    const T* ft = tables + 2 * Q * N;   // fold(B) | fold(D) follow the plain tables
-    for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = ft[t];
-  }
   if constexpr (ANISO) {   // the batch's Voigt matrices
     T* cs = smem + AnisoSmem<P, Q, T>::OFFC;
     for (int t = tid; t < ne * C21; t += NT) {
@@ -379,7 +405,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   }
 #if ELAS_L2_PREFETCH
   if (tid == 0 && pref_ctas > 0) {
-    const int64_t pe0 = e0 + (int64_t)pref_ctas * EB;
+    const int64_t pe0 = e0 + (int64_t)(PST ? (int)gridDim.x : pref_ctas) * EB;
     if (pe0 < e_end && !COLORED && !OTF) {   // (OTF: no quadrature data to prefetch)
       const int64_t pne = (e_end - pe0) < EB ? (e_end - pe0) : EB;
       const uintptr_t a0 = (uintptr_t)(qd + pe0 * (int64_t)C::QDE);
@@ -405,6 +431,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
     }
   }
 #endif
+  const bool zcol = tid < ne * N * N;
   __syncthreads();
 
   // ---------------- Stage Z: folded contraction in z of the gathered column -------------
@@ -527,7 +554,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   if constexpr (STG) {
     const uint32_t bar = smem_u32(mbar);
     asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(bar)
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(bar), "r"(phase)
         : "memory");
   }
   for (int w = tid; w < ne * Q * Q; w += NT) {
@@ -775,6 +802,9 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
       }
   }
   __syncthreads();
+  if constexpr (PST) {
+    if (batch + bstride < nbatch) gather(batch + bstride);   // in flight during stage Zt
+  }
 
   // ---------------- Stage Zt: folded transposed contraction in z + scatter-add ----------
   for (int w = tid; w < ne * N * N; w += NT) {
@@ -847,6 +877,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
       }
     }
   }
+  }   // batch loop
 }
 
 template <int P, int Q, typename T, bool COLORED, bool OTF = false, bool ANISO = false>
@@ -870,7 +901,9 @@ cudaError_t launch_apply_eo_pqc(const Slab& s, const double* x, double* y, const
   }
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
-  const int64_t grid = (ne + C::EB - 1) / C::EB;
+  const int64_t nb = (ne + C::EB - 1) / C::EB;
+  constexpr bool PST = PersistEO<P>::value && !COLORED && !OTF && !ANISO;
+  const int64_t grid = PST ? (nb < pref ? nb : pref) : nb;
   apply_eo_kernel<P, Q, T, COLORED, OTF, ANISO><<<(unsigned)grid, C::NT, SMEM, st>>>(
       x, y, static_cast<const T*>(qd), rr, static_cast<const T*>(tables), s, e_begin, e_end, pref, cm, cc);
   return cudaGetLastError();
