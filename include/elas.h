@@ -138,6 +138,12 @@ int elas_variant(const elas_op* op);
  * applies.  Returns ELAS_OK or ELAS_EINVAL / ELAS_ECUDA / ELAS_ENCCL. */
 int elas_apply(elas_op* op, const double* x, double* y);
 
+/* Accumulating apply y += A x (A as elas_apply applies it: y_c += x_c on constrained dofs), the
+ * semantics of SPEC.md's CPU program (y += A x) for smoothers that compose
+ * updates.  Single-GPU operators only (ELAS_EINVAL for nranks > 1).  Same layout, alignment,
+ * aliasing and stream rules as elas_apply. */
+int elas_apply_add(elas_op* op, const double* x, double* y);
+
 /* End-to-end form of elas_apply: x_host, y_host are HOST pointers (pinned recommended);
  * copies x to an op-owned device buffer, applies, copies y back, and synchronises the
  * op's stream.  Returns as elas_apply (ELAS_ENOMEM if the staging buffers fail). */

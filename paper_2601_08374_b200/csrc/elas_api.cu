@@ -630,6 +630,19 @@ int elas_apply(elas_op* op, const double* x, double* y) {
   return ELAS_OK;
 }
 
+int elas_apply_add(elas_op* op, const double* x, double* y) {
+  if (!op || !x || !y) { set_error("elas_apply_add: NULL argument"); return ELAS_EINVAL; }
+  if (x == y) { set_error("elas_apply_add: x and y must not alias"); return ELAS_EINVAL; }
+  if (((uintptr_t)x | (uintptr_t)y) & 7u) { set_error("elas_apply_add: x, y must be 8-byte aligned"); return ELAS_EINVAL; }
+  if (op->nranks != 1) {
+    set_error("elas_apply_add: single-GPU operators only (the interface sum needs the partial planes alone)");
+    return ELAS_EINVAL;
+  }
+  const Slab& s = op->slab;
+  CUDA_OR(elas::launch_face_add(s, x, y, op->stream), "face add launch");
+  return range_apply(op, x, y, 0, (int64_t)s.nx * s.ny * s.nz, op->stream);
+}
+
 int elas_interface_add(elas_op* op, double* y, const double* lo_halo, const double* hi_halo) {
   if (!op || !y) { set_error("elas_interface_add: NULL argument"); return ELAS_EINVAL; }
   if (!op->external) { set_error("elas_interface_add: only for external-exchange ops (nranks > 1, nccl_id NULL)"); return ELAS_EINVAL; }

@@ -170,7 +170,10 @@ cudaError_t launch_qdata(int p, int q, int layout, const Slab& s, const double* 
 // y = (I - Z) x on node planes [K0, K1): a memset of the planes plus a copy of x on the
 // constrained face nodes only (blockIdx.y = face); the general init_kernel computed node
 // coordinates for every dof (64-bit divisions) and cost ~25 % of an apply on Dirichlet meshes.
-__global__ void face_copy_kernel(Slab s, int K0, int K1, const double* __restrict__ x, double* __restrict__ y) {
+// add = 0: y = x on the constrained face nodes; add = 1: y += x, each node once (a node on several
+// constrained faces is handled by the lowest-numbered one)
+__global__ void face_copy_kernel(Slab s, int K0, int K1, const double* __restrict__ x, double* __restrict__ y,
+                                 int add) {
   const int face = blockIdx.y;
   if (!(s.faces & (1u << face))) return;
   const int axis = face >> 1, hi = face & 1;
@@ -193,7 +196,19 @@ __global__ void face_copy_kernel(Slab s, int K0, int K1, const double* __restric
     else if (axis == 1) { I = a; J = hi ? s.Ny - 1 : 0; K = k0 + b; }
     else { I = a; J = b; K = hi ? s.Nz - 1 : 0; }
     const int64_t idx = c * s.nodes + (int64_t)K * plane + (int64_t)J * s.Nx + I;
-    y[idx] = x[idx];
+    if (!add) {
+      y[idx] = x[idx];
+    } else {
+      bool lower = false;   // on a lower-numbered constrained face?
+      for (int f2 = 0; f2 < face; ++f2) {
+        if (!(s.faces & (1u << f2))) continue;
+        const int ax2 = f2 >> 1, hi2 = f2 & 1;
+        const int v = ax2 == 0 ? I : ax2 == 1 ? J : K;
+        const int vmax = ax2 == 0 ? s.Nx - 1 : ax2 == 1 ? s.Ny - 1 : s.Nz - 1;
+        if (v == (hi2 ? vmax : 0)) lower = true;
+      }
+      if (!lower) y[idx] += x[idx];
+    }
   }
 }
 
@@ -214,7 +229,14 @@ cudaError_t launch_init_planes(const Slab& s, int K0, int K1, const double* x, d
   }
   if (e != cudaSuccess || !s.faces) return e;
   const int64_t maxface = 3 * (int64_t)std::max(std::max(s.Nx, s.Ny), K1 - K0) * std::max(std::max(s.Ny, s.Nx), K1 - K0);
-  face_copy_kernel<<<dim3((unsigned)grid_for(maxface, 256), 6), 256, 0, st>>>(s, K0, K1, x, y);
+  face_copy_kernel<<<dim3((unsigned)grid_for(maxface, 256), 6), 256, 0, st>>>(s, K0, K1, x, y, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_face_add(const Slab& s, const double* x, double* y, cudaStream_t st) {
+  if (!s.faces) return cudaSuccess;
+  const int64_t m = std::max(std::max(s.Nx, s.Ny), s.Nz);
+  face_copy_kernel<<<dim3((unsigned)grid_for(3 * m * m, 256), 6), 256, 0, st>>>(s, 0, s.Nz, x, y, 1);
   return cudaGetLastError();
 }
 

@@ -30,7 +30,7 @@ EXPORTED = ["elas_create", "elas_apply", "elas_apply_host", "elas_interface_add"
             "elas_diagonal", "elas_cheb_create", "elas_cheb_lambda_max", "elas_cheb_apply",
             "elas_cheb_destroy", "elas_pcg", "elas_gmg_create", "elas_gmg_level_op", "elas_gmg_levels",
             "elas_gmg_set_stream", "elas_gmg_apply", "elas_pcg_gmg", "elas_gmg_destroy", "elas_gmg_transfer",
-            "elas_set_deterministic", "elas_dot", "elas_create_aniso"]
+            "elas_set_deterministic", "elas_dot", "elas_create_aniso", "elas_apply_add"]
 PC_NONE, PC_JACOBI, PC_CHEBYSHEV = 0, 1, 2
 
 
@@ -131,6 +131,8 @@ def load(path=None):
     lib.elas_pcg_gmg.argtypes = [P, P, P, P, ctypes.c_double, ctypes.c_int, ctypes.POINTER(elas_solve_report), D]
     lib.elas_create_aniso.restype = P
     lib.elas_create_aniso.argtypes = [ctypes.POINTER(elas_mesh), ctypes.c_int, ctypes.c_int, D]
+    lib.elas_apply_add.restype = ctypes.c_int
+    lib.elas_apply_add.argtypes = [P, P, P]
     lib.elas_dot.restype = ctypes.c_int
     lib.elas_dot.argtypes = [P, P, P, D]
     lib.elas_set_deterministic.restype = ctypes.c_int
@@ -247,6 +249,10 @@ def elas_create_ex(nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 
 
 def elas_apply(h, x, y):
     _check(load().elas_apply(h, _ptr(x), _ptr(y)), "elas_apply")
+
+
+def elas_apply_add(h, x, y):
+    _check(load().elas_apply_add(h, _ptr(x), _ptr(y)), "elas_apply_add")
 
 
 def elas_apply_host(h, x_host, y_host):
@@ -446,6 +452,10 @@ class Operator:
 
     def apply(self, x, y):
         elas_apply(self.h, x, y)
+
+    def apply_add(self, x, y):
+        """y += A x (single GPU)."""
+        elas_apply_add(self.h, x, y)
 
     def apply_host(self, x_host, y_host):
         elas_apply_host(self.h, x_host, y_host)

@@ -610,3 +610,22 @@ def test_anisotropic_isotropic_voigt_equals_isotropic_op():
     yi, ya = gpu_apply(P, op=op_i), gpu_apply(P, op=op_a)
     op_i.close(); op_a.close()
     assert rel_l2(ya, yi) <= 1e-13
+
+
+@pytest.mark.parametrize("faces,variant", [(0, 0), (63, 0), (1 | 8 | 16, 4), (63, 3), (2 | 32, 2)])
+def test_apply_add_accumulates(faces, variant):
+    """elas_apply_add: y += A x with identity rows counted once on edges/corners of several faces."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    p, q = (1, 3) if variant == 3 else (6, 8) if variant == 2 else (3, 5)
+    P = synth.make_problem("t", 3, 2, 4, p, q, perturb=True, lognormal_material=True, faces=faces, seed=81)
+    op = Operator.from_problem(P, variant=variant)
+    x = torch.from_numpy(P.x).cuda()
+    y0 = torch.from_numpy(synth.splitmix_uniform(P.num_dofs, 4)).cuda()
+    y = y0.clone()
+    op.apply_add(x, y)
+    Ax = torch.empty_like(x)
+    op.apply(x, Ax)
+    torch.cuda.synchronize()
+    op.close()
+    assert rel_l2((y - y0).cpu().numpy(), Ax.cpu().numpy()) <= 1e-14
