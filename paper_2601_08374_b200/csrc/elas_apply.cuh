@@ -142,20 +142,21 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // are in words of that size.
 constexpr int qd_stride_words(int q, int WB) { return WB == 8 ? (9 * q * q * q + 1) & ~1 : (9 * q * q * q + 3) & ~3; }
 
-template <int P, int Q, int TABSZ = 2 * Q * (P + 1), int NTHR = ELAS_NT, int WB = 8>
+// PAD = 0: unpadded tiles (minimal shared memory, bank conflicts accepted)
+template <int P, int Q, int TABSZ = 2 * Q * (P + 1), int NTHR = ELAS_NT, int WB = 8, int PAD = 1>
 struct Cfg {
   static constexpr int N = P + 1;
   static constexpr int NT = NTHR;
   static constexpr int G = 128 / WB;       // word-banks per wavefront
   static constexpr int AL = 16 / WB;       // words per 16 bytes
-  static constexpr int SA = pick_SA(N, Q, G);
+  static constexpr int SA = PAD ? pick_SA(N, Q, G) : N * N;
   static constexpr int ZV = Q * SA;        // variant stride (Zb | Zd)
   static constexpr int ZC = 2 * ZV;        // component stride
-  static constexpr int ZE = pick_ZE(N, Q, SA, pick_S2(N, Q, G), 3 * ZC, 9 * Q * pick_S2(N, Q, G), NT, G);  // element stride
-  static constexpr int S2 = pick_S2(N, Q, G);
+  static constexpr int S2 = PAD ? pick_S2(N, Q, G) : Q * N;
+  static constexpr int ZE = PAD ? pick_ZE(N, Q, SA, S2, 3 * ZC, 9 * Q * S2, NT, G) : 3 * ZC;  // element stride
   static constexpr int YV = Q * S2;        // variant stride (Y0 | Y1 | Y2)
   static constexpr int YC = 3 * YV;        // component stride
-  static constexpr int YE = pick_YE(N, Q, SA, S2, ZE, 3 * YC, NT, G);  // element stride
+  static constexpr int YE = PAD ? pick_YE(N, Q, SA, S2, ZE, 3 * YC, NT, G) : 3 * YC;  // element stride
   static constexpr int TAB = (TABSZ + AL - 1) & ~(AL - 1);  // coefficient tables (B then D, or folded)
   // elements per CTA: enough x-lines for every thread in stage X; at low order also enough
   // z-columns (N^2 per element) to keep every thread busy in stages Z and Zt.

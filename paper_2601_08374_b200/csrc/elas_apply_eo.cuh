@@ -99,8 +99,11 @@ template <int P> struct MinbEO32 {
 #endif
 template <int P> struct PersistEO { static constexpr bool value = ELAS_EO_PERSIST != 0 || P == 5; };
 
+#ifndef ELAS_EO_NOPAD_P
+#define ELAS_EO_NOPAD_P 0   // a degree whose tiles go unpadded (experiment knob; 0 = none)
+#endif
 template <int P, int Q, typename T = double>
-using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEO<P>::value, (int)sizeof(T)>;
+using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEO<P>::value, (int)sizeof(T), P == ELAS_EO_NOPAD_P ? 0 : 1>;
 
 // Quadrature-data ring (ELAS_QD_RING = R > 0): every stage-X thread owns one x-line (EB q^2 <=
 // NT), so it streams ITS line's 9 values per point into its own shared-memory slots with
