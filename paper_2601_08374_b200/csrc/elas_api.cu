@@ -48,6 +48,7 @@ DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
 #undef DECL
 #define DECL(P)                                                                                  \
   cudaError_t apply_eo_info_p##P(int q, int fp32, ApplyLaunch* info);                            \
+  cudaError_t apply_eo_upload_p##P(int q, const double* fold);                                   \
   cudaError_t apply_eo_launch_p##P(int q, int fp32, const Slab& s, const double* x, double* y,   \
                                    const void* qd, const double* rr, const void* tables,        \
                                    int64_t e_begin, int64_t e_end, cudaStream_t st, const int* color, \
@@ -85,6 +86,15 @@ cudaError_t apply_launch(int p, int q, const Slab& s, const double* x, double* y
 cudaError_t apply_eo_info(int p, int q, int fp32, ApplyLaunch* info) {
   switch (p) {
 #define CASE(P) case P: return apply_eo_info_p##P(q, fp32, info);
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t apply_eo_upload(int p, int q, const double* fold) {
+  switch (p) {
+#define CASE(P) case P: return apply_eo_upload_p##P(q, fold);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
     default: return cudaErrorInvalidValue;
@@ -251,6 +261,7 @@ int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* m
     if ((e = cudaMalloc(&op->tabf, sizeof(float) * tabf.size())) ||
         (e = cudaMemcpy(op->tabf, tabf.data(), sizeof(float) * tabf.size(), cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(op->tab, tabh.data(), sizeof(double) * tabh.size(), cudaMemcpyHostToDevice)) ||
+        (e = elas::apply_eo_upload(p, q, tabh.data() + 2 * q * (p + 1))) ||
         (e = cudaMemcpy(dV, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(dlam, lam.data(), sizeof(double) * ne, cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(dmu, muv.data(), sizeof(double) * ne, cudaMemcpyHostToDevice)) ||

@@ -278,6 +278,36 @@ __device__ __forceinline__ void pointwise_aniso(T (&g)[3][3], const T (&A)[9], c
       g[c][d] = fma(S[c][2], A[3 * d + 2], fma(S[c][1], A[3 * d + 1], S[c][0] * A[3 * d]));
 }
 
+// Folded tables in the CONSTANT bank (ELAS_EO_CTAB): every coefficient index of the folded
+// contractions is a compile-time constant after unrolling and warp-uniform, so ptxas fetches the
+// coefficients with uniform-datapath LDCU (SASS `LDCU.128 URx, c[0x3][imm]`) instead of per-thread
+// shared-memory loads, and the CTA prologue has no table copy.  The tables depend on (p, q) only (GLL nodes, Gauss points), so one
+// copy per (P, Q, T) serves every operator; apply_eo_upload_p<P> writes it at elas_create.
+// Per (degree, precision, geometry mode): 2 = every stage reads the constant bank, 1 = stages Z,
+// Y, Yt, Zt only (stage X, where the x-line's gradients hold most registers, keeps the shared-
+// memory copy), 0 = shared memory only.  Measured (config 4, GDoF/s, shared -> constant; FP64 /
+// FP32 / geometry on the fly): p2 (all stages) 16.7 -> 18.6 / 23.5 -> 24.7 / 13.0 -> 15.4
+// (anisotropic 12.3 -> 12.8);
+// stages Z/Y only: p3 22.2 -> 23.3 / 32.7 -> 34.3 / 20.7 -> 21.7, p4 26.2 -> 26.9 / 42.4 -> 43.4
+// / 22.9 -> 23.7, p5 30.1 -> 26.9 (lost) / 45.2 -> 45.9 / 26.0 -> 26.5, p6 33.4 -> 31.0 (lost) /
+// 50.6 -> 52.8 / 33.1 -> 31.4 (lost), p7, p8 lost everywhere; all stages at p3..p8 FP64 lost
+// 8-40 %.  Where it loses, the coefficients hoisted into registers push the register-capped
+// kernels into spills.  ELAS_EO_CTAB = 2 / 1 / -1 forces all stages / stages Z-Y / none.
+#ifndef ELAS_EO_CTAB
+#define ELAS_EO_CTAB 0
+#endif
+template <int P, typename T, bool OTF, bool ANISO>
+struct CtabEO {
+  static constexpr int tuned = P == 2 ? 2
+                               : ANISO          ? 0   // p3 19.8 -> 17.4, p4 22.0 -> 21.8 (stages Z/Y)
+                               : sizeof(T) == 4 ? (P >= 3 && P <= 6 ? 1 : 0)
+                               : OTF            ? (P >= 3 && P <= 5 ? 1 : 0)
+                                                : (P >= 3 && P <= 4 ? 1 : 0);
+  static constexpr int value = ELAS_EO_CTAB == 0 ? tuned : ELAS_EO_CTAB < 0 ? 0 : ELAS_EO_CTAB;
+};
+template <int P, int Q, typename T>
+__constant__ T c_fold[2 * Fold<P, Q>::TS];
+
 template <int P, int Q, typename T, bool COLORED, bool OTF = false, bool ANISO = false>
 __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<P>::value : MinbEO<P>::value)
     apply_eo_kernel(const double* __restrict__ x, double* __restrict__ y, const T* __restrict__ qd,
@@ -293,8 +323,12 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   constexpr bool STG = RG::STAGE && !OTF;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
-  T* tB = smem;            // folded B (parity +1)
-  T* tD = smem + F::TS;    // folded D (parity -1)
+  constexpr bool CT = CtabEO<P, T, OTF, ANISO>::value == 2;         // stage X tables in the constant bank
+  constexpr bool CZ = CtabEO<P, T, OTF, ANISO>::value >= 1;         // stages Z, Y, Yt, Zt
+  const T* tB = CZ ? c_fold<P, Q, T> : smem;                // folded B (parity +1)
+  const T* tD = CZ ? c_fold<P, Q, T> + F::TS : smem + F::TS;  // folded D (parity -1)
+  const T* xB = CT ? c_fold<P, Q, T> : smem;
+  const T* xD = CT ? c_fold<P, Q, T> + F::TS : smem + F::TS;
   T* sZ = smem + C::TAB;
   T* sY = sZ + EB * C::ZE;
   T* sQ = smem + C::BASE;
@@ -332,7 +366,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
     }
   };
   gather(blockIdx.x);
-  {
+  if constexpr (!CT) {
     const T* ft = tables + 2 * Q * N;   // fold(B) | fold(D) follow the plain tables
     for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = ft[t];
   }
@@ -569,7 +603,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
     T g[3][3][Q];
 #pragma unroll
     for (int v = 0; v < 3; ++v) {
-      const T* tab = (v == 0) ? tD : tB;   // x-derivative for v = 0 (parity -1)
+      const T* tab = (v == 0) ? xD : xB;   // x-derivative for v = 0 (parity -1)
       const bool odd = (v == 0);
       T fp[3][NE], fm[3][NHX];
       {
@@ -693,7 +727,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
     }
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      const T* tab = (d == 0) ? tD : tB;
+      const T* tab = (d == 0) ? xD : xB;
       const bool odd = (d == 0);
       // fold over the points a1 in place: g[.][a] <- g_a + g_{q-1-a}, g[.][q-1-a] <- g_a - g_{q-1-a}
 #pragma unroll
@@ -938,12 +972,31 @@ void info_eo_pq(ApplyLaunch* info) {
 
 }  // namespace elas
 
+// write the folded tables (host, 2 * TS doubles: fold(B) | fold(D)) into the constant bank of
+// the FP64 and FP32 instances
+namespace elas {
+template <int P, int Q>
+cudaError_t upload_eo_pq(const double* fold) {
+  constexpr int n = 2 * Fold<P, Q>::TS;
+  float f[n];
+  for (int i = 0; i < n; ++i) f[i] = (float)fold[i];
+  cudaError_t e = cudaMemcpyToSymbol(c_fold<P, Q, double>, fold, sizeof(double) * n);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_fold<P, Q, float>, f, sizeof(float) * n);
+  return e;
+}
+}  // namespace elas
+
 #define ELAS_DEFINE_DEGREE_EO(P)                                                                \
   namespace elas {                                                                              \
   cudaError_t apply_eo_info_p##P(int q, int fp32, ApplyLaunch* info) {                          \
     if (q == P + 1) fp32 ? info_eo_pq<P, P + 1, float>(info) : info_eo_pq<P, P + 1, double>(info); \
     else if (q == P + 2) fp32 ? info_eo_pq<P, P + 2, float>(info) : info_eo_pq<P, P + 2, double>(info); \
     else return cudaErrorInvalidValue;                                                          \
+    return cudaSuccess;                                                                         \
+  }                                                                                             \
+  cudaError_t apply_eo_upload_p##P(int q, const double* fold) {                                 \
+    if (q == P + 1) return upload_eo_pq<P, P + 1>(fold);                                        \
+    if (q == P + 2) return upload_eo_pq<P, P + 2>(fold);                                        \
     return cudaSuccess;                                                                         \
   }                                                                                             \
   cudaError_t apply_eo_launch_p##P(int q, int fp32, const Slab& s, const double* x, double* y,  \

@@ -39,6 +39,8 @@ cudaError_t apply_eo_info(int p, int q, int fp32, ApplyLaunch* info);
 // iz0}: the linear range [e_begin, e_end) of one color's element lattice, plain-RMW scatter.
 // otf = 1: geometry on the fly (FP64 only; qd = geo[e][GEO_WORDS], QD_LAYOUT_OTF)
 // cc != nullptr: anisotropic material (21 Voigt words per element; FP64 only)
+// folded tables (2 * fold_table_size doubles) into the folded kernels' constant bank (ELAS_EO_CTAB)
+cudaError_t apply_eo_upload(int p, int q, const double* fold);
 cudaError_t apply_eo_launch(int p, int q, int fp32, const Slab& s, const double* x, double* y, const void* qd,
                             const double* rr, const void* tables, int64_t e_begin, int64_t e_end,
                             cudaStream_t st, const int* color = nullptr, int otf = 0, const double* cc = nullptr);
