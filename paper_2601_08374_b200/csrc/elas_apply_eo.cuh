@@ -283,26 +283,27 @@ __device__ __forceinline__ void pointwise_aniso(T (&g)[3][3], const T (&A)[9], c
 // coefficients with uniform-datapath LDCU (SASS `LDCU.128 URx, c[0x3][imm]`) instead of per-thread
 // shared-memory loads, and the CTA prologue has no table copy.  The tables depend on (p, q) only (GLL nodes, Gauss points), so one
 // copy per (P, Q, T) serves every operator; apply_eo_upload_p<P> writes it at elas_create.
-// Per (degree, precision, geometry mode): 2 = every stage reads the constant bank, 1 = stages Z,
-// Y, Yt, Zt only (stage X, where the x-line's gradients hold most registers, keeps the shared-
-// memory copy), 0 = shared memory only.  Measured (config 4, GDoF/s, shared -> constant; FP64 /
+// Per (degree, precision, geometry mode) a mask of the stages that read the constant bank:
+// 1 = forward Z, Y; 2 = X; 4 = transposed Yt, Zt (7 = all; 5 = all but stage X, where the
+// x-line's gradients hold most registers); the others read the shared-memory copy.  Measured (config 4, GDoF/s, shared -> constant; FP64 /
 // FP32 / geometry on the fly): p2 (all stages) 16.7 -> 18.6 / 23.5 -> 24.7 / 13.0 -> 15.4
 // (anisotropic 12.3 -> 12.8);
 // stages Z/Y only: p3 22.2 -> 23.3 / 32.7 -> 34.3 / 20.7 -> 21.7, p4 26.2 -> 26.9 / 42.4 -> 43.4
 // / 22.9 -> 23.7, p5 30.1 -> 26.9 (lost) / 45.2 -> 45.9 / 26.0 -> 26.5, p6 33.4 -> 31.0 (lost) /
 // 50.6 -> 52.8 / 33.1 -> 31.4 (lost), p7, p8 lost everywhere; all stages at p3..p8 FP64 lost
-// 8-40 %.  Where it loses, the coefficients hoisted into registers push the register-capped
-// kernels into spills.  ELAS_EO_CTAB = 2 / 1 / -1 forces all stages / stages Z-Y / none.
+// 8-40 %; forward stages only (mask 1): FP64 p4 26.8 -> 27.2, p6 33.4 -> 31.7, config 5
+// 33.5 -> 31.9; forward + X (mask 3): FP32 p4 43.5 -> 44.4.  Where it loses, the coefficients hoisted into registers push the register-capped
+// kernels into spills.  ELAS_EO_CTAB = mask / -1 overrides (experiments).
 #ifndef ELAS_EO_CTAB
 #define ELAS_EO_CTAB 0
 #endif
 template <int P, typename T, bool OTF, bool ANISO>
 struct CtabEO {
-  static constexpr int tuned = P == 2 ? 2
+  static constexpr int tuned = P == 2 ? 7
                                : ANISO          ? 0   // p3 19.8 -> 17.4, p4 22.0 -> 21.8 (stages Z/Y)
-                               : sizeof(T) == 4 ? (P >= 3 && P <= 6 ? 1 : 0)
-                               : OTF            ? (P >= 3 && P <= 5 ? 1 : 0)
-                                                : (P >= 3 && P <= 4 ? 1 : 0);
+                               : sizeof(T) == 4 ? (P == 4 ? 3 : P >= 3 && P <= 6 ? 5 : 0)
+                               : OTF            ? (P >= 3 && P <= 5 ? 5 : 0)
+                                                : (P == 3 ? 5 : P == 4 ? 1 : 0);
   static constexpr int value = ELAS_EO_CTAB == 0 ? tuned : ELAS_EO_CTAB < 0 ? 0 : ELAS_EO_CTAB;
 };
 template <int P, int Q, typename T>
@@ -323,12 +324,14 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   constexpr bool STG = RG::STAGE && !OTF;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
-  constexpr bool CT = CtabEO<P, T, OTF, ANISO>::value == 2;         // stage X tables in the constant bank
-  constexpr bool CZ = CtabEO<P, T, OTF, ANISO>::value >= 1;         // stages Z, Y, Yt, Zt
-  const T* tB = CZ ? c_fold<P, Q, T> : smem;                // folded B (parity +1)
-  const T* tD = CZ ? c_fold<P, Q, T> + F::TS : smem + F::TS;  // folded D (parity -1)
-  const T* xB = CT ? c_fold<P, Q, T> : smem;
-  const T* xD = CT ? c_fold<P, Q, T> + F::TS : smem + F::TS;
+  constexpr int CTM = CtabEO<P, T, OTF, ANISO>::value;   // constant-bank stages (mask, above)
+  constexpr bool CT = (CTM & 7) == 7;                     // no stage reads the shared copy
+  const T* tB = (CTM & 1) ? c_fold<P, Q, T> : smem;       // stages Z, Y: folded B (parity +1)
+  const T* tD = (CTM & 1) ? c_fold<P, Q, T> + F::TS : smem + F::TS;  // folded D (parity -1)
+  const T* xB = (CTM & 2) ? c_fold<P, Q, T> : smem;       // stage X
+  const T* xD = (CTM & 2) ? c_fold<P, Q, T> + F::TS : smem + F::TS;
+  const T* bB = (CTM & 4) ? c_fold<P, Q, T> : smem;       // stages Yt, Zt
+  const T* bD = (CTM & 4) ? c_fold<P, Q, T> + F::TS : smem + F::TS;
   T* sZ = smem + C::TAB;
   T* sY = sZ + EB * C::ZE;
   T* sQ = smem + C::BASE;
@@ -802,8 +805,8 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
 #pragma unroll
       for (int j = 0; j < NE; ++j) {
         const bool jmid = (N & 1) && j == NH;
-        const T be = tB[F::BE + j * QE + a];
-        const T de = tD[F::BE + j * QE + a];
+        const T be = bB[F::BE + j * QE + a];
+        const T de = bD[F::BE + j * QE + a];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           bX[c][j] = fma(be, v0p[c], bX[c][j]);
@@ -811,8 +814,8 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
           if (!jmid) bY[c][j] = fma(de, v1p[c], bY[c][j]);
         }
         if (!mid) {
-          const T bo = tB[F::BO + j * QH + a];
-          const T dO = tD[F::BO + j * QH + a];
+          const T bo = bB[F::BO + j * QH + a];
+          const T dO = bD[F::BO + j * QH + a];
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             bX[c][j] = fma(dO, v1m[c], bX[c][j]);
@@ -873,16 +876,16 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
 #pragma unroll
       for (int k = 0; k < NE; ++k) {
         const bool kmid = (N & 1) && k == NH;
-        const T be = tB[F::BE + k * QE + a];
-        const T de = tD[F::BE + k * QE + a];
+        const T be = bB[F::BE + k * QE + a];
+        const T de = bD[F::BE + k * QE + a];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           X[c][k] = fma(be, wbp[c], X[c][k]);
           if (!kmid) Y[c][k] = fma(de, wdp[c], Y[c][k]);
         }
         if (!mid) {
-          const T bo = tB[F::BO + k * QH + a];
-          const T dO = tD[F::BO + k * QH + a];
+          const T bo = bB[F::BO + k * QH + a];
+          const T dO = bD[F::BO + k * QH + a];
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             X[c][k] = fma(dO, wdm[c], X[c][k]);
