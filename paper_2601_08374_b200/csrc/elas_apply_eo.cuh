@@ -285,14 +285,17 @@ __device__ __forceinline__ void pointwise_aniso(T (&g)[3][3], const T (&A)[9], c
 // copy per (P, Q, T) serves every operator; apply_eo_upload_p<P> writes it at elas_create.
 // Per (degree, precision, geometry mode) a mask of the stages that read the constant bank:
 // 1 = forward Z, Y; 2 = X; 4 = transposed Yt, Zt (7 = all; 5 = all but stage X, where the
-// x-line's gradients hold most registers); the others read the shared-memory copy.  Measured (config 4, GDoF/s, shared -> constant; FP64 /
+// x-line's gradients hold most registers); the others read the shared-memory copy, which the
+// prologue fills from the constant bank with bit 8 set, else from global memory.  Measured (config 4, GDoF/s, shared -> constant; FP64 /
 // FP32 / geometry on the fly): p2 (all stages) 16.7 -> 18.6 / 23.5 -> 24.7 / 13.0 -> 15.4
 // (anisotropic 12.3 -> 12.8);
 // stages Z/Y only: p3 22.2 -> 23.3 / 32.7 -> 34.3 / 20.7 -> 21.7, p4 26.2 -> 26.9 / 42.4 -> 43.4
 // / 22.9 -> 23.7, p5 30.1 -> 26.9 (lost) / 45.2 -> 45.9 / 26.0 -> 26.5, p6 33.4 -> 31.0 (lost) /
 // 50.6 -> 52.8 / 33.1 -> 31.4 (lost), p7, p8 lost everywhere; all stages at p3..p8 FP64 lost
 // 8-40 %; forward stages only (mask 1): FP64 p4 26.8 -> 27.2, p6 33.4 -> 31.7, config 5
-// 33.5 -> 31.9; forward + X (mask 3): FP32 p4 43.5 -> 44.4.  Where it loses, the coefficients hoisted into registers push the register-capped
+// 33.5 -> 31.9; forward + X (mask 3): FP32 p4 43.5 -> 44.4.  Prologue fill from the constant
+// bank (bit 8) on top: FP64 p3 23.3 -> 23.7 (13), p4 27.3 -> 27.6 (9), p6 33.4 -> 33.6, p7 23.3 ->
+// 23.5, p8 29.4 -> 29.6 (8); on the fly p5 26.5 -> 27.1 (13); FP32 no gain.  Where it loses, the coefficients hoisted into registers push the register-capped
 // kernels into spills.  ELAS_EO_CTAB = mask / -1 overrides (experiments).
 #ifndef ELAS_EO_CTAB
 #define ELAS_EO_CTAB 0
@@ -300,10 +303,10 @@ __device__ __forceinline__ void pointwise_aniso(T (&g)[3][3], const T (&A)[9], c
 template <int P, typename T, bool OTF, bool ANISO>
 struct CtabEO {
   static constexpr int tuned = P == 2 ? 7
-                               : ANISO          ? 0   // p3 19.8 -> 17.4, p4 22.0 -> 21.8 (stages Z/Y)
+                               : ANISO          ? 8   // p3 19.8 -> 17.4, p4 22.0 -> 21.8 (stages Z/Y)
                                : sizeof(T) == 4 ? (P == 4 ? 3 : P >= 3 && P <= 6 ? 5 : 0)
-                               : OTF            ? (P >= 3 && P <= 5 ? 5 : 0)
-                                                : (P == 3 ? 5 : P == 4 ? 1 : 0);
+                               : OTF            ? (P >= 3 && P <= 5 ? 13 : 8)
+                                                : (P == 3 ? 13 : P == 4 ? 9 : 8);
   static constexpr int value = ELAS_EO_CTAB == 0 ? tuned : ELAS_EO_CTAB < 0 ? 0 : ELAS_EO_CTAB;
 };
 template <int P, int Q, typename T>
@@ -369,7 +372,11 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
     }
   };
   gather(blockIdx.x);
-  if constexpr (!CT) {
+  if constexpr (!CT && (CTM & 8)) {
+    // the shared copy filled from the constant bank: LDC does not queue behind the gather's
+    // DRAM misses in L1TEX the way the global table loads do
+    for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = c_fold<P, Q, T>[t];
+  } else if constexpr (!CT) {
     const T* ft = tables + 2 * Q * N;   // fold(B) | fold(D) follow the plain tables
     for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = ft[t];
   }
