@@ -629,3 +629,22 @@ def test_apply_add_accumulates(faces, variant):
     torch.cuda.synchronize()
     op.close()
     assert rel_l2((y - y0).cpu().numpy(), Ax.cpu().numpy()) <= 1e-14
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 6])
+def test_coexisting_operators_constant_tables(p):
+    """The folded kernels read their 1D tables from a per-(p, q, precision) constant bank written at
+    elas_create: operators of both quadrature orders and both precisions,
+    created before any of them applies, each still match the oracle."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator, VARIANT_FOLDED, VARIANT_FOLDED_F32, VARIANT_FOLDED_OTF
+    probs = [synth.make_problem(f"ct_p{p}_q{p + dq}", 3, 2, 2, p, p + dq, perturb=True,
+                                lognormal_material=True, faces=1 | 16, seed=40 + dq) for dq in (1, 2)]
+    ops = [(P, v, Operator.from_problem(P, variant=v)) for P in probs
+           for v in (VARIANT_FOLDED, VARIANT_FOLDED_F32, VARIANT_FOLDED_OTF)]
+    for P, v, op in reversed(ops):
+        y = gpu_apply(P, op=op)
+        tol = TOL_F32 if v == VARIANT_FOLDED_F32 else TOL
+        assert rel_l2(y, oracle.apply(oracle_mesh(P), P.x)) <= tol, (P.name, v)
+    for _, _, op in ops:
+        op.close()
