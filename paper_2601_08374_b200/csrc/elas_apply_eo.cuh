@@ -295,8 +295,12 @@ __device__ __forceinline__ void pointwise_aniso(T (&g)[3][3], const T (&A)[9], c
 // 8-40 %; forward stages only (mask 1): FP64 p4 26.8 -> 27.2, p6 33.4 -> 31.7, config 5
 // 33.5 -> 31.9; forward + X (mask 3): FP32 p4 43.5 -> 44.4.  Prologue fill from the constant
 // bank (bit 8) on top: FP64 p3 23.3 -> 23.7 (13), p4 27.3 -> 27.6 (9), p6 33.4 -> 33.6, p7 23.3 ->
-// 23.5, p8 29.4 -> 29.6 (8); on the fly p5 26.5 -> 27.1 (13); FP32 no gain.  Where it loses, the coefficients hoisted into registers push the register-capped
-// kernels into spills.  ELAS_EO_CTAB = mask / -1 overrides (experiments).
+// 23.5, p8 29.4 -> 29.6 (8); on the fly p5 26.5 -> 27.1 (13); FP32 no gain.  Per-thread LDC into
+// general registers (bit 16) for stage X (mask 26): FP32 p5 46.0 -> 47.8, FP64 p8 29.7 -> 30.1,
+// on the fly p7 22.0 -> 22.3; every other degree loses 1-15 % (one LDC issued per coefficient use;
+// all stages: p6 33.6 -> 31.9).  Where the constant bank loses, the coefficients hoisted into
+// registers push the register-capped kernels into spills, and a DFMA with a uniform-register
+// operand issues at about half rate.  ELAS_EO_CTAB = mask / -1 overrides.
 #ifndef ELAS_EO_CTAB
 #define ELAS_EO_CTAB 0
 #endif
@@ -304,9 +308,9 @@ template <int P, typename T, bool OTF, bool ANISO>
 struct CtabEO {
   static constexpr int tuned = P == 2 ? 7
                                : ANISO          ? 8   // p3 19.8 -> 17.4, p4 22.0 -> 21.8 (stages Z/Y)
-                               : sizeof(T) == 4 ? (P == 4 ? 3 : P >= 3 && P <= 6 ? 5 : 0)
-                               : OTF            ? (P >= 3 && P <= 5 ? 13 : 8)
-                                                : (P == 3 ? 13 : P == 4 ? 9 : 8);
+                               : sizeof(T) == 4 ? (P == 4 ? 3 : P == 5 ? 26 : P >= 3 && P <= 6 ? 5 : 0)
+                               : OTF            ? (P >= 3 && P <= 5 ? 13 : P == 7 ? 26 : 8)
+                                                : (P == 3 ? 13 : P == 4 ? 9 : P == 8 ? 26 : 8);
   static constexpr int value = ELAS_EO_CTAB == 0 ? tuned : ELAS_EO_CTAB < 0 ? 0 : ELAS_EO_CTAB;
 };
 template <int P, int Q, typename T>
@@ -329,12 +333,16 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   T* smem = reinterpret_cast<T*>(smem_raw);
   constexpr int CTM = CtabEO<P, T, OTF, ANISO>::value;   // constant-bank stages (mask, above)
   constexpr bool CT = (CTM & 7) == 7;                     // no stage reads the shared copy
-  const T* tB = (CTM & 1) ? c_fold<P, Q, T> : smem;       // stages Z, Y: folded B (parity +1)
-  const T* tD = (CTM & 1) ? c_fold<P, Q, T> + F::TS : smem + F::TS;  // folded D (parity -1)
-  const T* xB = (CTM & 2) ? c_fold<P, Q, T> : smem;       // stage X
-  const T* xD = (CTM & 2) ? c_fold<P, Q, T> + F::TS : smem + F::TS;
-  const T* bB = (CTM & 4) ? c_fold<P, Q, T> : smem;       // stages Yt, Zt
-  const T* bD = (CTM & 4) ? c_fold<P, Q, T> + F::TS : smem + F::TS;
+  // bit 16: per-thread LDC into general registers (the offset is zero at run time but not provably
+  // warp-uniform, so ptxas cannot route the coefficient through a uniform register: DFMA keeps
+  // all-register operands, and the coefficients stay off the shared-memory pipe)
+  const int cz = (CTM & 16) ? (int)threadIdx.x * (int)(gridDim.z - 1) : 0;
+  const T* tB = (CTM & 1) ? c_fold<P, Q, T> + cz : smem;  // stages Z, Y: folded B (parity +1)
+  const T* tD = (CTM & 1) ? c_fold<P, Q, T> + F::TS + cz : smem + F::TS;  // folded D (parity -1)
+  const T* xB = (CTM & 2) ? c_fold<P, Q, T> + cz : smem;  // stage X
+  const T* xD = (CTM & 2) ? c_fold<P, Q, T> + F::TS + cz : smem + F::TS;
+  const T* bB = (CTM & 4) ? c_fold<P, Q, T> + cz : smem;  // stages Yt, Zt
+  const T* bD = (CTM & 4) ? c_fold<P, Q, T> + F::TS + cz : smem + F::TS;
   T* sZ = smem + C::TAB;
   T* sY = sZ + EB * C::ZE;
   T* sQ = smem + C::BASE;
