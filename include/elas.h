@@ -78,7 +78,9 @@ typedef struct {
  * tables (GLL nodes, Gauss-Legendre rule, Lagrange values/derivatives; host), copies the
  * vertices of this rank's slab to the device and runs the quadrature-data setup kernel
  * (J, det J, A = J^{-1}, W = w det J; stores A~ = sqrt(mu_e W) A per point and
- * r_e = lambda_e / mu_e per element).  Synchronises.  lambda/mu: HOST pointers.
+ * r_e = lambda_e / mu_e per element), and writes the folded 1D tables of (p, q) into the
+ * folded kernels' constant bank on the current device (identical bytes for every operator of
+ * that (p, q), so concurrent creates are safe).  Synchronises.  lambda/mu: HOST pointers.
  * q must be p+1 or p+2.  Host arrays are copied; the caller may free them on return.
  * Returns NULL on error (see elas_last_error). */
 elas_op* elas_create(const elas_mesh* mesh, int p, int q, const double* lambda, const double* mu);
