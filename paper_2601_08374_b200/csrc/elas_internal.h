@@ -101,6 +101,8 @@ cudaError_t launch_qdata(int p, int q, int layout, const Slab& s, const double* 
 cudaError_t launch_init(const Slab& s, const double* x, double* y, cudaStream_t st);
 cudaError_t launch_init_planes(const Slab& s, int K0, int K1, const double* x, double* y, cudaStream_t st);
 // y += x on the constrained dofs (each once): the identity rows of the accumulating apply
+// y = x on every constrained row (whole slab)
+cudaError_t launch_face_copy(const Slab& s, const double* x, double* y, cudaStream_t st);
 cudaError_t launch_face_add(const Slab& s, const double* x, double* y, cudaStream_t st);
 cudaError_t launch_plane_add(const Slab& s, int which_plane, double* y, const double* halo,
                              cudaStream_t st);

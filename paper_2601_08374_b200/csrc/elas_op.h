@@ -24,6 +24,8 @@ struct elas_op {
   double* ys = nullptr;
   cudaStream_t h2d = nullptr, d2h = nullptr;   // copy streams of the chunked host apply
   std::vector<cudaEvent_t> host_ev;            // per chunk: x landed, chunk computed
+  cudaStream_t init_stream = nullptr;          // pipelined y zeroing of elas_apply (high priority)
+  std::vector<cudaEvent_t> init_ev;            // per z-chunk: its node planes zeroed
   cudaStream_t stream = nullptr;
   // multi-GPU
   ncclComm_t comm = nullptr;

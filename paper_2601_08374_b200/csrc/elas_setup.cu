@@ -233,6 +233,13 @@ cudaError_t launch_init_planes(const Slab& s, int K0, int K1, const double* x, d
   return cudaGetLastError();
 }
 
+cudaError_t launch_face_copy(const Slab& s, const double* x, double* y, cudaStream_t st) {
+  if (!s.faces) return cudaSuccess;
+  const int64_t m = std::max(std::max(s.Nx, s.Ny), s.Nz);
+  face_copy_kernel<<<dim3((unsigned)grid_for(3 * m * m, 256), 6), 256, 0, st>>>(s, 0, s.Nz, x, y, 0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_face_add(const Slab& s, const double* x, double* y, cudaStream_t st) {
   if (!s.faces) return cudaSuccess;
   const int64_t m = std::max(std::max(s.Nx, s.Ny), s.Nz);

@@ -648,3 +648,35 @@ def test_coexisting_operators_constant_tables(p):
         assert rel_l2(y, oracle.apply(oracle_mesh(P), P.x)) <= tol, (P.name, v)
     for _, _, op in ops:
         op.close()
+
+
+@pytest.mark.parametrize("p,dims,faces", [(1, (64, 64, 64), 63), (2, (40, 41, 161), 1 | 16 | 32), (3, (48, 40, 150), 2 | 8)])
+def test_pipelined_zeroing_chunk_planes(p, dims, faces):
+    """Large operators (>= 2^18 elements, the size where elas_apply may pipeline the zeroing of
+    y over 8 z-chunks, ELAS_INIT_CHUNKS): rows on the eighth-planes (chunk boundaries), on the
+    Dirichlet faces and at random match the oracle; identity rows are exact; applying into a y
+    that already holds a result overwrites all of it."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    nx, ny, nz = dims
+    P = synth.make_problem("pz", nx, ny, nz, p, p + 1, perturb=True, lognormal_material=True, faces=faces, seed=77)
+    assert P.num_elements >= 1 << 18
+    Nx, Ny, Nz = P.node_dims
+    N = Nx * Ny * Nz
+    chunk_planes = [((k * nz) // 8) * p for k in range(1, 8)]
+    extra = np.concatenate([plane_rows(P, K + d, 24, K + d) for K in chunk_planes for d in (-1, 0, 1)]
+                           + [np.arange(0, N, Nx)[:40]])
+    rows = sample_rows(P, 256, 3, extra=extra)
+    op = Operator.from_problem(P)
+    xd = torch.from_numpy(P.x).cuda()
+    yd = torch.full_like(xd, 1e300)
+    op.apply(xd, yd)
+    op.apply(xd, yd)          # y already holds a result: the chunked zeroing must clear all of it
+    torch.cuda.synchronize()
+    y = yd.cpu().numpy()
+    op.close()
+    m = oracle_mesh(P)
+    assert rel_l2(y[rows], oracle.apply_rows(m, P.x, rows)) <= TOL
+    Z = oracle.constrained_mask(m)
+    assert np.array_equal(y[Z], P.x[Z])
+    assert np.all(np.abs(y) < 1e100)
