@@ -246,6 +246,52 @@ def sweep_config4(reps=10, warmup=3, variant=0, ps=range(1, 9)):
     return out
 
 
+# ------------------------------------------------------------------------------ ablation (Table 4)
+
+def ablation_bench(p=8, reps=3, warmup=2):
+    """The paper's ablation (Table 4: p = 8, 51.17M DoF) on B200 at config 4,
+    p = 8 (50.9M DoF): per-apply time of each optimization stage and the marginal speedups.
+    Stages 0-2 are the unfused pipelines (ELAS_VARIANT_ABL_*), 3 the fused SIMT kernel, 4 the
+    folded kernel (AUTO)."""
+    import torch
+    import synth
+    from paper_2601_08374_b200.elas import (Operator, VARIANT_ABL_PA, VARIANT_ABL_SF, VARIANT_ABL_VOIGT,
+                                            VARIANT_SIMT, VARIANT_FOLDED)
+    P = synth.make_config(4, p)
+    x = torch.from_numpy(P.x).cuda()
+    y = torch.empty_like(x)
+    stages = [("PA (baseline, Alg. 1: unfused, dense O(p^6) contractions)", VARIANT_ABL_PA),
+              ("+ Sum Factorization (C1)", VARIANT_ABL_SF), ("+ Voigt Notation (C2)", VARIANT_ABL_VOIGT),
+              ("+ Kernel Fusion (C3)", VARIANT_SIMT), ("+ Loop Structure (B200: folded kernel)", VARIANT_FOLDED)]
+    paper = [None, 12.74, 1.01, 2.15, 1.96]
+    rows, prev = [], None
+    for (name, v), pm in zip(stages, paper):
+        op = Operator.from_problem(P, variant=v)
+        for _ in range(warmup):
+            op.apply(x, y)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            op.apply(x, y)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        rows.append({"stage": name, "variant": v, "ms_per_apply": round(ms, 4),
+                     "gdofs": round(P.num_dofs / (ms / 1e3) / 1e9, 3),
+                     "marginal_speedup": None if prev is None else round(prev / ms, 2),
+                     "paper_kernel_marginal_speedup": pm})
+        prev = ms
+        op.close()
+        torch.cuda.empty_cache()
+    del x, y
+    torch.cuda.empty_cache()
+    return {"workload": f"config 4, p = {p} (q = {P.q}, {P.num_dofs} DoF); paper: Kunpeng 920, p = 8, 51.17M DoF "
+                        "(kernel column of Table 4, context only)",
+            "stages": rows, "overall_speedup": round(rows[0]["ms_per_apply"] / rows[-1]["ms_per_apply"], 2),
+            "paper_overall_kernel_speedup": 54.19}
+
+
 # ------------------------------------------------------------------------------ config 2 hot / cold
 
 def small_configs(reps=20):
@@ -613,6 +659,8 @@ def run_ours(args):
         line["config2_hot_cold"] = config2_hot_cold()
         line["configs_1_3"] = small_configs()
         line["anisotropic"] = anisotropic_sweep()
+    if ws == 1 and not args.no_sweep:
+        line["ablation"] = ablation_bench()
     if ws == 1 and not args.no_solver:
         line["solver"] = solver_bench()
     if ws == 1 and not args.no_sweep:

@@ -109,6 +109,16 @@ elas_op* elas_create_aniso(const elas_mesh* mesh, int p, int q, const double* C2
  *   ELAS_VARIANT_FOLDED_OTF  the folded FP64 kernel with GEOMETRY ON THE FLY: no stored
  *                       quadrature data (40 doubles per element instead of 9 q^3); A~ rebuilt
  *                       at every point from the trilinear map.
+ *   ELAS_VARIANT_ABL_PA, ELAS_VARIANT_ABL_SF, ELAS_VARIANT_ABL_VOIGT  the paper's ablation
+ *                       stages (Table 4) on B200, for measurement: unfused
+ *                       gather / gradient / pointwise / transposed-contraction / scatter
+ *                       kernels with the element vectors and QVec in HBM; PA = dense O(p^6)
+ *                       basis-gradient contractions (Alg. 1), SF = sum factorisation (C1),
+ *                       VOIGT = SF + 6-component stress in QVec (C2).  "+ fusion" (C3) and
+ *                       "+ loop structure" are ELAS_VARIANT_SIMT and ELAS_VARIANT_FOLDED.  Same
+ *                       results to rounding; scratch of (6 n^3 + 9 q^3) doubles per element is
+ *                       allocated at the first apply.  No deterministic
+ *                       mode.
  *   ELAS_VARIANT_AUTO   the faster measured variant for (p, q).
  * The choice fixes the quadrature-data layout, so it is made at creation. */
 #define ELAS_VARIANT_AUTO 0
@@ -118,6 +128,9 @@ elas_op* elas_create_aniso(const elas_mesh* mesh, int p, int q, const double* C2
 #define ELAS_VARIANT_FOLDED 4
 #define ELAS_VARIANT_FOLDED_F32 5
 #define ELAS_VARIANT_FOLDED_OTF 6
+#define ELAS_VARIANT_ABL_PA 7
+#define ELAS_VARIANT_ABL_SF 8
+#define ELAS_VARIANT_ABL_VOIGT 9
 
 /* elas_create with an explicit kernel variant; NULL + ELAS_EINVAL message if the variant
  * does not exist for (p, q). */

@@ -170,6 +170,10 @@ void free_op(elas_op* op) {
   for (cudaEvent_t ev : op->prof_ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : op->host_ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : op->init_ev) cudaEventDestroy(ev);
+  cudaFree(op->abl_E);
+  cudaFree(op->abl_Eo);
+  cudaFree(op->abl_Q);
+  cudaFree(op->abl_G);
   if (op->init_stream) cudaStreamDestroy(op->init_stream);
   if (op->h2d) cudaStreamDestroy(op->h2d);
   if (op->d2h) cudaStreamDestroy(op->d2h);
@@ -334,6 +338,8 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
                                 op->variant == ELAS_VARIANT_FOLDED_F32 ? (const void*)op->tabf : (const void*)op->tab,
                                 0, cnt, st, cm, op->variant == ELAS_VARIANT_FOLDED_OTF, op->cc);
     }
+  } else if (op->variant >= ELAS_VARIANT_ABL_PA) {
+    e = elas::ablation_apply(op, op->variant - ELAS_VARIANT_ABL_PA, x, y, e0, e1, st);
   } else
   e = op->variant == ELAS_VARIANT_TENSOR
                       ? elas::apply_tc_launch(op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
@@ -426,7 +432,7 @@ elas_op* elas_create(const elas_mesh* m, int p, int q, const double* lambda, con
 
 elas_op* elas_create_ex(const elas_mesh* m, int p, int q, const double* lambda, const double* mu, int variant) {
   elas::g_err.clear();
-  if (variant < ELAS_VARIANT_AUTO || variant > ELAS_VARIANT_FOLDED_OTF) {
+  if (variant < ELAS_VARIANT_AUTO || variant > ELAS_VARIANT_ABL_VOIGT) {
     set_error("elas_create_ex: unknown variant");
     return nullptr;
   }
@@ -582,6 +588,7 @@ int elas_set_deterministic(elas_op* op, int on) {
 // kernels of ONE element range [z0, z1) of layers: 1, or the non-empty colors in colored mode
 static int range_launches(const elas_op* op, int z0, int z1) {
   if (z1 <= z0) return 0;
+  if (op->variant >= ELAS_VARIANT_ABL_PA) return 5;   // gather, gradient, pointwise, transpose, scatter
   if (!op->deterministic) return 1;
   const Slab& s = op->slab;
   int n = 0;

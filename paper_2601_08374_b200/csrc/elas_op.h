@@ -24,6 +24,7 @@ struct elas_op {
   double* ys = nullptr;
   cudaStream_t h2d = nullptr, d2h = nullptr;   // copy streams of the chunked host apply
   std::vector<cudaEvent_t> host_ev;            // per chunk: x landed, chunk computed
+  double *abl_E = nullptr, *abl_Eo = nullptr, *abl_Q = nullptr, *abl_G = nullptr;   // ablation-stage scratch
   cudaStream_t init_stream = nullptr;          // pipelined y zeroing of elas_apply (high priority)
   std::vector<cudaEvent_t> init_ev;            // per z-chunk: its node planes zeroed
   cudaStream_t stream = nullptr;
@@ -67,4 +68,7 @@ int pcg_core(elas_op* op, int kind, const PrecondFn& M, const double* b, double*
 // exchange the partial interface planes of y with the neighbour ranks and add them (NCCL mode,
 // synchronous on the op's stream); no-op for nranks == 1 or external mode
 int exchange_planes(elas_op* op, double* y);
+// the paper's ablation stages 0 (PA), 1 (+SF), 2 (+Voigt) over elements [e0, e1) (elas_ablation.cu)
+cudaError_t ablation_apply(elas_op* op, int stage, const double* x, double* y, int64_t e0, int64_t e1,
+                           cudaStream_t st);
 }  // namespace elas

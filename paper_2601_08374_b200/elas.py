@@ -20,6 +20,8 @@ LIB_PATH = os.path.join(HERE, "lib", os.environ.get("ELAS_LIBNAME", "libelas.so"
 
 VARIANT_AUTO, VARIANT_SIMT, VARIANT_TENSOR, VARIANT_THREAD, VARIANT_FOLDED, VARIANT_FOLDED_F32, VARIANT_FOLDED_OTF = (
     0, 1, 2, 3, 4, 5, 6)
+# the paper's ablation stages (Table 4) as unfused pipelines, for measurement (include/elas.h)
+VARIANT_ABL_PA, VARIANT_ABL_SF, VARIANT_ABL_VOIGT = 7, 8, 9
 ELAS_OK, ELAS_EINVAL, ELAS_EGEOM, ELAS_ENOMEM, ELAS_ECUDA, ELAS_ENCCL = 0, -1, -2, -3, -4, -5
 FACE_XMIN, FACE_XMAX, FACE_YMIN, FACE_YMAX, FACE_ZMIN, FACE_ZMAX = 1, 2, 4, 8, 16, 32
 

@@ -1,5 +1,10 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "pipelined or config5 or config4 or launches or apply_host or dirichlet" > gpurun_out/pz_tests.log 2>&1; tail -3 gpurun_out/pz_tests.log
-bash tools/ab_libs.sh 0 2 4 6 > gpurun_out/ab_ic.txt 2>&1
-for L in libelas.so libt_ic1.so libt_ic16.so libelas.so libt_ic1.so; do ELAS_LIBNAME=$L timeout 300 python tools/ab_cfg5.py 4 2>&1 | tail -1; done >> gpurun_out/ab_ic.txt
-cat gpurun_out/ab_ic.txt
+timeout 900 python -m pytest tests/test_gpu_ablation.py -q -x > gpurun_out/abl_tests.log 2>&1; tail -2 gpurun_out/abl_tests.log
+timeout 600 python -c "
+import bench, json
+r = bench.ablation_bench()
+print(json.dumps([(s['stage'][:30], s['ms_per_apply'], s['marginal_speedup']) for s in r['stages']]), r['overall_speedup'])
+r = bench.ablation_bench(p=4)
+print(json.dumps([(s['stage'][:30], s['ms_per_apply'], s['marginal_speedup']) for s in r['stages']]), r['overall_speedup'])
+"
+timeout 600 python tools/abl_breakdown.py 8 2>/dev/null
