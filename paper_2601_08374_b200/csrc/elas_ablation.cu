@@ -28,7 +28,8 @@ namespace elas {
 namespace abl {
 
 constexpr int NTE = 256;   // element-wise kernels
-constexpr int NTC = 256;   // one CTA per element
+// threads of the one-CTA-per-element kernels: 512 where an element's stage has >= 4096 fibres
+template <int N, int QQ> struct Ntc { static constexpr int value = 9 * QQ * QQ * N >= 4096 ? 512 : 256; };
 
 __host__ __device__ inline int64_t grid_of(int64_t n, int nt) {
   const int64_t g = (n + nt - 1) / nt;
@@ -208,15 +209,15 @@ __global__ void point_kernel(const double* __restrict__ qd, const double* __rest
 //   Y1[c][d][a3][a2][i] = sum_j (d == 1 ? D : B)[a2][j] Z1[c][d == 2][a3][j][i]
 //   G[c][d](a1, a2, a3) = sum_i (d == 0 ? D : B)[a1][i] Y1[c][d][a3][a2][i]   -> Q[e][pt][3c + d]
 template <int N, int QQ>
-__global__ void __launch_bounds__(NTC) grad_sf_kernel(const double* __restrict__ E, const double* __restrict__ tab,
+__global__ void __launch_bounds__(Ntc<N, QQ>::value) grad_sf_kernel(const double* __restrict__ E, const double* __restrict__ tab,
                                                       double* __restrict__ Q, int64_t e0) {
   extern __shared__ double sm[];
-  constexpr int n = N, q = QQ, n2 = n * n, n3 = n2 * n, q2 = q * q, q3 = q2 * q;
+  constexpr int n = N, q = QQ, n2 = n * n, n3 = n2 * n, q2 = q * q, q3 = q2 * q, NTC = Ntc<N, QQ>::value;
   double* B = sm;
   double* D = B + q * n;
-  double* u = D + q * n;          // 3 n^3
-  double* Z1 = u + 3 * n3;        // 3 * 2 * q * n^2
-  double* Y1 = Z1 + 6 * q * n2;   // 3 * 3 * q^2 * n
+  double* Z1 = D + q * n;         // 3 * 2 * q * n^2
+  double* u = Z1 + 6 * q * n2;    // 3 n^3, dead after stage Z ...
+  double* Y1 = u;                 // ... so stage Y writes over it (3 * 3 * q^2 * n)
   const int64_t e = e0 + blockIdx.x;
   for (int t = threadIdx.x; t < 2 * q * n; t += NTC) sm[t] = tab[t];
   for (int t = threadIdx.x; t < 3 * n3; t += NTC) u[t] = E[e * 3 * n3 + t];
@@ -259,11 +260,11 @@ __global__ void __launch_bounds__(NTC) grad_sf_kernel(const double* __restrict__
 //   T2[c][zk][a3][j][i] = zk = 0: sum_a2 B[a2][j] T1[c][0] + D[a2][j] T1[c][1];  zk = 1: sum_a2 B[a2][j] T1[c][2]
 //   Eo[c][k][j][i]      = sum_a3 B[a3][k] T2[c][0] + D[a3][k] T2[c][1]
 template <int N, int QQ>
-__global__ void __launch_bounds__(NTC) div_sf_kernel(const double* __restrict__ Q, const double* __restrict__ qd,
+__global__ void __launch_bounds__(Ntc<N, QQ>::value) div_sf_kernel(const double* __restrict__ Q, const double* __restrict__ qd,
                                                      const double* __restrict__ tab, double* __restrict__ Eo, int voigt,
                                                      int64_t e0) {
   extern __shared__ double sm[];
-  constexpr int n = N, q = QQ, n2 = n * n, n3 = n2 * n, q2 = q * q, q3 = q2 * q;
+  constexpr int n = N, q = QQ, n2 = n * n, n3 = n2 * n, q2 = q * q, q3 = q2 * q, NTC = Ntc<N, QQ>::value;
   double* B = sm;
   double* D = B + q * n;
   double* F = D + q * n;          // [c][d][pt], 9 q^3
@@ -325,7 +326,10 @@ __global__ void __launch_bounds__(NTC) div_sf_kernel(const double* __restrict__ 
   }
 }
 
-size_t grad_sf_smem(int n, int q) { return sizeof(double) * (2 * q * n + 3 * n * n * n + 6 * q * n * n + 9 * q * q * n); }
+size_t grad_sf_smem(int n, int q) {
+  const int un = 3 * n * n * n > 9 * q * q * n ? 3 * n * n * n : 9 * q * q * n;   // u and Y1 share
+  return sizeof(double) * (2 * q * n + 6 * q * n * n + un);
+}
 size_t div_sf_smem(int n, int q) { return sizeof(double) * (2 * q * n + 9 * q * q * q + 9 * q * q * n + 6 * q * n * n); }
 
 template <int N, int QQ>
@@ -343,12 +347,12 @@ cudaError_t run_stage(const elas_op* op, int stage, const double* x, double* y, 
   if (stage == 0)
     grad_dense_kernel<N, QQ><<<(unsigned)grid_of(nel * q3, NTE), NTE, 0, st>>>(op->abl_E, op->abl_G, op->abl_Q, e0, e1);
   else
-    grad_sf_kernel<N, QQ><<<(unsigned)nel, NTC, grad_sf_smem(N, QQ), st>>>(op->abl_E, op->tab, op->abl_Q, e0);
+    grad_sf_kernel<N, QQ><<<(unsigned)nel, Ntc<N, QQ>::value, grad_sf_smem(N, QQ), st>>>(op->abl_E, op->tab, op->abl_Q, e0);
   point_kernel<QQ><<<(unsigned)grid_of(nel * q3, NTE), NTE, 0, st>>>(op->qd, op->rr, op->abl_Q, stage >= 2, e0, e1);
   if (stage == 0)
     div_dense_kernel<N, QQ><<<(unsigned)grid_of(nel * 3 * n3, NTE), NTE, 0, st>>>(op->abl_Q, op->abl_G, op->abl_Eo, e0, e1);
   else
-    div_sf_kernel<N, QQ><<<(unsigned)nel, NTC, div_sf_smem(N, QQ), st>>>(op->abl_Q, op->qd, op->tab, op->abl_Eo,
+    div_sf_kernel<N, QQ><<<(unsigned)nel, Ntc<N, QQ>::value, div_sf_smem(N, QQ), st>>>(op->abl_Q, op->qd, op->tab, op->abl_Eo,
                                                                          stage >= 2, e0);
   scatter_kernel<N><<<(unsigned)grid_of(nel * 3 * n3, NTE), NTE, 0, st>>>(s, op->abl_Eo, y, e0, e1);
   return cudaGetLastError();
