@@ -253,8 +253,15 @@ int elas_pcg(elas_op* op, int precond, elas_cheb* cheb, const double* b, double*
  * host.  This is the reduction elas_pcg and the power iteration use. */
 int elas_dot(elas_op* op, const double* a, const double* b, double* result);
 
-/* Geometric multigrid V-cycle (Sec. 3, Fig. 2),
- * single-GPU (nranks == 1).  Readings R22-R25 in DESIGN.md.
+/* Geometric multigrid V-cycle (Sec. 3, Fig. 2).
+ * Readings R22-R25 in DESIGN.md.  Z-slabs (fine->nranks > 1): nz must be divisible by
+ * nranks * 2^(levels-1) so every level's slabs align (coarse slab = fine slab / 2); every level
+ * is a slab op of the same rank; with fine->nccl_id the finest level owns the communicator and
+ * the coarser levels borrow it, restriction counts a shared fine interface plane on the rank
+ * below only and sums the coarse interface planes over NCCL, and the V-cycle runs eagerly (no
+ * graph capture); without nccl_id (external-exchange mode) only elas_gmg_transfer works, and a
+ * restriction leaves the coarse interface planes as LOCAL partial sums (complete them with
+ * elas_interface_add on elas_gmg_level_op(g, level + 1)); apply / pcg_gmg return ELAS_EINVAL.
  * create: builds `levels` levels from `fine` (same p, q; h-coarsening by 2 per axis: nx, ny, nz
  *   divisible by 2^(levels-1); coarse vertices = fine vertices of even index; per-element
  *   lambda, mu averaged over the 8 children; same Dirichlet faces), each an elas_op of kernel

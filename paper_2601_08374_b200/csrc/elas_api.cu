@@ -163,7 +163,7 @@ void free_op(elas_op* op) {
   cudaFree(op->ys);
   cudaFree(op->halo_lo);
   cudaFree(op->halo_hi);
-  if (op->comm) ncclCommDestroy(op->comm);
+  if (op->comm && !op->comm_borrowed) ncclCommDestroy(op->comm);
   if (op->comm_stream) cudaStreamDestroy(op->comm_stream);
   if (op->ev_boundary) cudaEventDestroy(op->ev_boundary);
   if (op->ev_comm) cudaEventDestroy(op->ev_comm);
@@ -364,6 +364,20 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
 }  // namespace
 
 namespace elas {
+
+int attach_comm(elas_op* op, ncclComm_t comm) {
+  if (!op || !comm || op->nranks < 2 || !op->external) {
+    set_error("attach_comm: needs an external-mode slab operator and a communicator");
+    return ELAS_EINVAL;
+  }
+  CUDA_OR(cudaStreamCreateWithFlags(&op->comm_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  CUDA_OR(cudaEventCreateWithFlags(&op->ev_boundary, cudaEventDisableTiming), "cudaEventCreate");
+  CUDA_OR(cudaEventCreateWithFlags(&op->ev_comm, cudaEventDisableTiming), "cudaEventCreate");
+  op->comm = comm;
+  op->comm_borrowed = true;
+  op->external = false;
+  return ELAS_OK;
+}
 
 int exchange_planes(elas_op* op, double* y) {
   if (op->nranks == 1 || op->external) return ELAS_OK;

@@ -94,8 +94,10 @@ __global__ void prolong_axis_kernel(const double* __restrict__ in, double* __res
 // out (dims `od`, axis extent nc p + 1) = transposed 1D prolongation along `axis` of `in`
 // (axis extent 2 nc p + 1): out[I_c] = sum over the fine nodes I_f owned by an element containing
 // I_c of M[t][i] in[I_f]
+// skip0: leave out fine index 0 along the axis (a slab's lower interface plane, owned by the rank
+// below, whose restriction already counts it)
 __global__ void restrict_axis_kernel(const double* __restrict__ in, double* __restrict__ out, Dims od, int axis,
-                                     const double* __restrict__ M, int p, int nc) {
+                                     const double* __restrict__ M, int p, int nc, int skip0) {
   const int64_t n0 = od.d[0], n1 = od.d[1], n2 = od.d[2];
   const int64_t total = 3 * n0 * n1 * n2;
   int64_t id[3] = {n0, n1, n2};
@@ -115,7 +117,7 @@ __global__ void restrict_axis_kernel(const double* __restrict__ in, double* __re
       const int k = (int)(Ic - e * p);
       if (k < 0 || k > p) continue;
       const int tmax = (e == nc - 1) ? 2 * p : 2 * p - 1;      // the owner rule of the prolongation
-      for (int tt = 0; tt <= tmax; ++tt) {
+      for (int tt = (skip0 && e == 0) ? 1 : 0; tt <= tmax; ++tt) {
         j[axis] = 2 * p * e + tt;
         acc = fma(M[tt * (p + 1) + k], in[j[0] + id[0] * (j[1] + id[1] * (j[2] + id[2] * c))], acc);
       }
@@ -159,11 +161,19 @@ int restrict_to(elas_gmg* g, int l, const double* fine, double* coarse) {
   cudaStream_t st = g->ops[l]->stream;
   const int p = g->p;
   Dims d1{{c.Nx, f.Ny, f.Nz}}, d2{{c.Nx, c.Ny, f.Nz}}, d3{{c.Nx, c.Ny, c.Nz}};
-  restrict_axis_kernel<<<gblocks(3 * d1.d[0] * d1.d[1] * d1.d[2]), 256, 0, st>>>(fine, g->ta[l], d1, 0, g->M1, p, c.nx);
-  restrict_axis_kernel<<<gblocks(3 * d2.d[0] * d2.d[1] * d2.d[2]), 256, 0, st>>>(g->ta[l], g->tb[l], d2, 1, g->M1, p, c.ny);
-  restrict_axis_kernel<<<gblocks(3 * d3.d[0] * d3.d[1] * d3.d[2]), 256, 0, st>>>(g->tb[l], coarse, d3, 2, g->M1, p, c.nz);
-  if (c.faces) mask_kernel<<<gblocks(3 * c.nodes), 256, 0, st>>>(coarse, c);
+  // z-slabs: the fine vector is replicated on the interface planes; only the owner (the rank below)
+  // counts a shared fine plane, and the coarse interface planes are then summed over the
+  // neighbours like the apply's (exchange_planes; the caller does it in external mode)
+  const int skip0 = g->ops[l]->rank > 0 ? 1 : 0;
+  restrict_axis_kernel<<<gblocks(3 * d1.d[0] * d1.d[1] * d1.d[2]), 256, 0, st>>>(fine, g->ta[l], d1, 0, g->M1, p, c.nx, 0);
+  restrict_axis_kernel<<<gblocks(3 * d2.d[0] * d2.d[1] * d2.d[2]), 256, 0, st>>>(g->ta[l], g->tb[l], d2, 1, g->M1, p, c.ny, 0);
+  restrict_axis_kernel<<<gblocks(3 * d3.d[0] * d3.d[1] * d3.d[2]), 256, 0, st>>>(g->tb[l], coarse, d3, 2, g->M1, p, c.nz,
+                                                                                skip0);
   GK(cudaGetLastError(), "restriction kernels");
+  int rc;
+  if ((rc = exchange_planes(g->ops[l + 1], coarse))) return rc;
+  if (c.faces) mask_kernel<<<gblocks(3 * c.nodes), 256, 0, st>>>(coarse, c);
+  GK(cudaGetLastError(), "restriction mask");
   return ELAS_OK;
 }
 
@@ -207,6 +217,7 @@ int vcycle(elas_gmg* g, int l, const double* b, double* x) {
 
 int vcycle_graph(elas_gmg* g, const double* b, double* x) {
   if (g->coarse_rtol > 0.0) return vcycle(g, 0, b, x);        // synchronising coarse solve: eager
+  if (g->ops[0]->nranks > 1) return vcycle(g, 0, b, x);       // z-slabs (NCCL inside): eager
   cudaStream_t user = g->ops[0]->stream;
   int rc;
   if (!g->gexec || g->gb != b || g->gx != x) {
@@ -260,9 +271,12 @@ elas_gmg* elas_gmg_create(const elas_mesh* fine, int p, int q, const double* lam
                           double coarse_rtol, int coarse_maxit, int variant) {
   using elas::set_error;
   if (!fine || !lambda || !mu) { set_error("elas_gmg_create: NULL argument"); return nullptr; }
-  if (fine->nranks > 1) { set_error("elas_gmg_create: single-GPU meshes only (nranks == 1)"); return nullptr; }
   if (levels < 1 || coarse_maxit < 1) { set_error("elas_gmg_create: need levels >= 1 and coarse_maxit >= 1"); return nullptr; }
   const int f = 1 << (levels - 1);
+  if (fine->nranks > 1 && fine->nz % (fine->nranks * f)) {
+    set_error("elas_gmg_create: z-slabs need nz divisible by nranks * 2^(levels-1) (aligned slabs on every level)");
+    return nullptr;
+  }
   if (fine->nx % f || fine->ny % f || fine->nz % f) {
     set_error("elas_gmg_create: nx, ny, nz must be divisible by 2^(levels-1)");
     return nullptr;
@@ -280,9 +294,14 @@ elas_gmg* elas_gmg_create(const elas_mesh* fine, int p, int q, const double* lam
     V.assign(fine->vertices, fine->vertices + (size_t)(fine->nx + 1) * (fine->ny + 1) * (fine->nz + 1) * 3);
   for (int l = 0; l < levels; ++l) {
     m.vertices = fine->vertices ? V.data() : nullptr;
+    m.nccl_id = l == 0 ? fine->nccl_id : nullptr;   // coarser slab levels borrow the finest communicator
     elas_op* op = elas_create_ex(&m, p, q, lam.data(), muv.data(), variant);
     if (!op) { elas::free_gmg(g); return nullptr; }
     g->ops.push_back(op);
+    if (l > 0 && fine->nccl_id && fine->nranks > 1 && elas::attach_comm(op, g->ops[0]->comm)) {
+      elas::free_gmg(g);
+      return nullptr;
+    }
     if (l == levels - 1) break;
     // next level
     const int nx = m.nx / 2, ny = m.ny / 2, nz = m.nz / 2;
@@ -320,7 +339,8 @@ elas_gmg* elas_gmg_create(const elas_mesh* fine, int p, int q, const double* lam
     m.nz = nz;
   }
   // smoothers (and the coarse preconditioner) + work vectors
-  for (int l = 0; l < levels; ++l) {
+  // (external-exchange slabs: transfers only, no smoothers -- their dots cannot be reduced)
+  for (int l = 0; l < levels && !g->ops[0]->external; ++l) {
     elas_cheb* ch = elas_cheb_create(g->ops[l], order, alpha, beta, power_iters, nullptr, seed);
     if (!ch) { elas::free_gmg(g); return nullptr; }
     g->chebs.push_back(ch);
@@ -391,14 +411,19 @@ int elas_gmg_transfer(elas_gmg* g, int level, int restrict_, const double* in, d
 int elas_gmg_apply(elas_gmg* g, const double* b, double* x) {
   if (!g || !b || !x) { elas::set_error("elas_gmg_apply: NULL argument"); return ELAS_EINVAL; }
   if (b == x) { elas::set_error("elas_gmg_apply: b and x must not alias"); return ELAS_EINVAL; }
+  if (g->ops[0]->external) {
+    elas::set_error("elas_gmg_apply: external-exchange slabs support transfers only (the V-cycle needs NCCL)");
+    return ELAS_EINVAL;
+  }
   return elas::vcycle_graph(g, b, x);
 }
 
 int elas_pcg_gmg(elas_op* op, elas_gmg* g, const double* b, double* x, double rtol, int maxit,
                  elas_solve_report* rep, double* history) {
   if (!op || !g || !b || !x) { elas::set_error("elas_pcg_gmg: NULL argument"); return ELAS_EINVAL; }
-  if (op->nranks != 1 || g->ops[0]->slab.nodes != op->slab.nodes || g->ops[0]->stream != op->stream) {
-    elas::set_error("elas_pcg_gmg: the V-cycle's finest level must match op (vector length, stream)");
+  if (op->nranks != g->ops[0]->nranks || op->rank != g->ops[0]->rank || op->external || g->ops[0]->external ||
+      g->ops[0]->slab.nodes != op->slab.nodes || g->ops[0]->stream != op->stream) {
+    elas::set_error("elas_pcg_gmg: the V-cycle's finest level must match op (slab, vector length, stream; NCCL mode)");
     return ELAS_EINVAL;
   }
   if (b == x || maxit < 0 || !(rtol >= 0.0)) { elas::set_error("elas_pcg_gmg: need b != x, maxit >= 0, rtol >= 0"); return ELAS_EINVAL; }

@@ -30,6 +30,7 @@ struct elas_op {
   cudaStream_t stream = nullptr;
   // multi-GPU
   ncclComm_t comm = nullptr;
+  bool comm_borrowed = false;        // a coarser GMG level sharing the finest level's communicator
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_boundary = nullptr, ev_comm = nullptr;
   double* halo_lo = nullptr;
@@ -68,6 +69,9 @@ int pcg_core(elas_op* op, int kind, const PrecondFn& M, const double* b, double*
 // exchange the partial interface planes of y with the neighbour ranks and add them (NCCL mode,
 // synchronous on the op's stream); no-op for nranks == 1 or external mode
 int exchange_planes(elas_op* op, double* y);
+// make an external-mode slab op (nranks > 1, no communicator) an NCCL-mode op on a borrowed
+// communicator (GMG levels share the finest level's); the op does not destroy it
+int attach_comm(elas_op* op, ncclComm_t comm);
 // the paper's ablation stages 0 (PA), 1 (+SF), 2 (+Voigt) over elements [e0, e1) (elas_ablation.cu)
 cudaError_t ablation_apply(elas_op* op, int stage, const double* x, double* y, int64_t e0, int64_t e1,
                            cudaStream_t st);

@@ -368,8 +368,8 @@ def elas_pcg(h, precond, cheb, b, x, rtol, maxit, history=False):
 
 def elas_gmg_create(nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0), faces=0, levels=2,
                     order=3, alpha=0.1, beta=1.1, power_iters=10, seed=1, coarse_rtol=-1.0, coarse_maxit=20,
-                    variant=VARIANT_AUTO):
-    m, lam_a, mu_a, keep = _mesh_args(nx, ny, nz, lam, mu, vertices, lengths, faces, 0, 1, None)
+                    variant=VARIANT_AUTO, rank=0, nranks=1, nccl_id=None):
+    m, lam_a, mu_a, keep = _mesh_args(nx, ny, nz, lam, mu, vertices, lengths, faces, rank, nranks, nccl_id)
     g = load().elas_gmg_create(ctypes.byref(m), p, q, _dptr(lam_a), _dptr(mu_a), levels, order, alpha, beta,
                                power_iters, seed, coarse_rtol, coarse_maxit, int(variant))
     if not g:
@@ -531,9 +531,9 @@ class GMG:
 
     def __init__(self, nx, ny, nz, p, q, lam, mu, vertices=None, lengths=(1.0, 1.0, 1.0), faces=0, levels=2,
                  order=3, alpha=0.1, beta=1.1, power_iters=10, seed=1, coarse_rtol=-1.0, coarse_maxit=20,
-                 variant=VARIANT_AUTO, stream=None):
+                 variant=VARIANT_AUTO, stream=None, rank=0, nranks=1, nccl_id=None):
         self.h = elas_gmg_create(nx, ny, nz, p, q, lam, mu, vertices, lengths, faces, levels, order, alpha, beta,
-                                 power_iters, seed, coarse_rtol, coarse_maxit, variant)
+                                 power_iters, seed, coarse_rtol, coarse_maxit, variant, rank, nranks, nccl_id)
         if stream is None:
             import torch
             stream = torch.cuda.current_stream()

@@ -164,3 +164,62 @@ def test_fp64_pcg_with_fp32_vcycle():
     op.apply(x, Ax)
     assert float(torch.linalg.norm(Ax - b) / torch.linalg.norm(b)) <= 1e-8
     g32.close(); g64.close(); op.close()
+
+
+@pytest.mark.parametrize("nranks,p,levels", [(2, 2, 2), (4, 1, 3), (2, 6, 2)])
+def test_slab_transfers_loopback(nranks, p, levels):
+    """Z-slab GMG (external-exchange mode, P slab hierarchies on ONE GPU): prolongation is local and
+    equals the single-GPU one on every slab; restriction counts a shared fine interface plane on
+    the rank below only, and after the coarse interface planes are summed with the library's
+    plane-add (elas_interface_add) it equals the single-GPU restriction.  The NCCL mode runs the
+    same kernels with exchange_planes doing that sum."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import GMG, elas_interface_add
+    f = 1 << (levels - 1)
+    nz = nranks * f * 2
+    P = synth.make_problem("sg", f, 2 * f, nz, p, p + 1, perturb=True, lognormal_material=True,
+                           faces=1 | 16 | 32, seed=61)
+    g = GMG.from_problem(P, levels=levels)
+    gs = [GMG.from_problem(P, levels=levels, rank=r, nranks=nranks) for r in range(nranks)]
+    rng = np.random.default_rng(5)
+    for lvl in range(levels - 1):
+        fo, co = g.level_op(lvl), g.level_op(lvl + 1)
+        nf, nc = g.level_dofs(lvl), g.level_dofs(lvl + 1)
+        Nf, Nc = nf // 3, nc // 3
+        nzf, nzc = nz >> lvl, nz >> (lvl + 1)
+        pf, pc = Nf // (nzf * p + 1), Nc // (nzc * p + 1)          # nodes per plane
+        vf = torch.from_numpy(rng.uniform(-1, 1, nf)).cuda()
+        vc = torch.from_numpy(rng.uniform(-1, 1, nc)).cuda()
+        rf_full, pc_full = torch.empty(nc, dtype=torch.float64, device="cuda"), torch.empty_like(vf)
+        g.transfer(lvl, True, vf, rf_full)
+        g.transfer(lvl, False, vc, pc_full)
+        parts, outs = [], []
+        for r in range(nranks):
+            zf0, zf1 = r * nzf // nranks, (r + 1) * nzf // nranks
+            zc0, zc1 = r * nzc // nranks, (r + 1) * nzc // nranks
+            vfl = vf.view(3, -1, pf)[:, zf0 * p:zf1 * p + 1].contiguous().reshape(-1)
+            vcl = vc.view(3, -1, pc)[:, zc0 * p:zc1 * p + 1].contiguous().reshape(-1)
+            assert vfl.numel() == gs[r].level_dofs(lvl) and vcl.numel() == gs[r].level_dofs(lvl + 1)
+            rl = torch.empty_like(vcl)
+            pl = torch.empty_like(vfl)
+            gs[r].transfer(lvl, True, vfl, rl)
+            gs[r].transfer(lvl, False, vcl, pl)
+            torch.cuda.synchronize()
+            # prolongation: local, equal to the full one on the slab
+            ref = pc_full.view(3, -1, pf)[:, zf0 * p:zf1 * p + 1].reshape(-1)
+            assert torch.allclose(pl, ref, rtol=0, atol=1e-13 * float(ref.abs().max()))
+            parts.append((rl.view(3, -1, pc)[:, 0].contiguous(), rl.view(3, -1, pc)[:, -1].contiguous()))
+            outs.append((rl, zc0, zc1))
+        for r, (rl, zc0, zc1) in enumerate(outs):
+            lo = parts[r - 1][1] if r > 0 else None
+            hi = parts[r + 1][0] if r < nranks - 1 else None
+            elas_interface_add(gs[r].level_op(lvl + 1), rl, lo, hi)
+        torch.cuda.synchronize()
+        for rl, zc0, zc1 in outs:
+            ref = rf_full.view(3, -1, pc)[:, zc0 * p:zc1 * p + 1].reshape(-1)
+            assert torch.allclose(rl, ref, rtol=0, atol=1e-13 * float(rf_full.abs().max()))
+    with pytest.raises(Exception):       # the V-cycle needs NCCL in slab mode
+        gs[0].apply(torch.zeros(gs[0].local_dofs, dtype=torch.float64, device="cuda"),
+                    torch.zeros(gs[0].local_dofs, dtype=torch.float64, device="cuda"))
+    for h in gs + [g]:
+        h.close()

@@ -103,3 +103,12 @@ def test_invalid_material_rejected_before_any_device_work():
     mu[1, 0, 1] = -0.5
     with pytest.raises(elas.ElasError, match="element 5"):
         elas.elas_create(2, 2, 2, 2, 4, lam, mu)
+
+
+def test_gmg_slab_alignment_rejected_before_any_device_work():
+    """Z-slab GMG needs every level's slabs aligned: nz divisible by nranks * 2^(levels-1)."""
+    from paper_2601_08374_b200 import elas
+    with pytest.raises(elas.ElasError, match="nranks"):
+        elas.elas_gmg_create(2, 2, 12, 2, 4, 1.0, 1.0, levels=3, rank=0, nranks=2)   # 12 % 8 != 0
+    with pytest.raises(elas.ElasError, match="divisible"):
+        elas.elas_gmg_create(2, 3, 8, 2, 4, 1.0, 1.0, levels=2)                       # ny odd
