@@ -491,6 +491,7 @@ elas_op* elas_create_ex(const elas_mesh* m, int p, int q, const double* lambda, 
   if (elas_slab_range(m->nz, op->rank, op->nranks, &b, &e) != ELAS_OK) { free_op(op); return nullptr; }
   op->ez0 = b;
   op->ez1 = e;
+  op->nz_global = m->nz;
   cudaGetDevice(&op->device);
   int rc = build(op, m, lambda, mu);
   if (rc != ELAS_OK) { free_op(op); return nullptr; }

@@ -12,6 +12,7 @@ struct elas_op {
   int variant = ELAS_VARIANT_SIMT;  // resolved kernel variant
   bool deterministic = false;       // colored scatter (elas_set_deterministic)
   int32_t ez0 = 0, ez1 = 0;
+  int32_t nz_global = 0;              // element layers of the whole mesh (all slabs)
   elas::Slab slab{};
   int device = 0;
   bool external = false;            // nranks > 1 without a communicator

@@ -358,9 +358,14 @@ __global__ void pcg_direction_kernel(double* __restrict__ p, const double* __res
 __global__ void copy_scalar_kernel(double* S, int dst, int src) { S[dst] = S[src]; }
 
 // default power-iteration start vector: splitmix64 counter generator (synth.splitmix_uniform)
-__global__ void splitmix_kernel(double* __restrict__ v, int64_t n, unsigned long long seed) {
+// indexed by the GLOBAL dof: a slab's vector is the slice of the one-GPU vector (replicated
+// interface planes identical on both ranks); nodes / nodes_g local / global nodes per
+// component, off = first global node of the slab
+__global__ void splitmix_kernel(double* __restrict__ v, int64_t n, unsigned long long seed, int64_t nodes,
+                                int64_t nodes_g, int64_t off) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    unsigned long long z = seed + (unsigned long long)(t + 1) * 0x9E3779B97F4A7C15ull;
+    const int64_t tg = (t / nodes) * nodes_g + off + t % nodes;
+    unsigned long long z = seed + (unsigned long long)(tg + 1) * 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
     z ^= z >> 31;
@@ -581,7 +586,12 @@ elas_cheb* elas_cheb_create(elas_op* op, int order, double alpha, double beta, i
   const int g = elas::grid_for(n);
   double* S = op->red + elas::RED_BLOCKS;
   if (v0) e = cudaMemcpyAsync(w, v0, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
-  else elas::splitmix_kernel<<<g, 256, 0, st>>>(w, n, seed);
+  else {
+    const elas::Slab& sl = op->slab;
+    const int64_t plane = (int64_t)sl.Nx * sl.Ny;
+    const int64_t nodes_g = plane * ((int64_t)op->nz_global * op->p + 1);
+    elas::splitmix_kernel<<<g, 256, 0, st>>>(w, n, seed, sl.nodes, nodes_g, plane * (int64_t)op->ez0 * op->p);
+  }
   if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return bail(e, "power iteration start vector");
   if (elas::dot(op, w, w, elas::S_NRM)) return bail(cudaSuccess, "");
   elas::normalize_kernel<<<g, 256, 0, st>>>(v, w, S + elas::S_NRM, n);
