@@ -9,8 +9,15 @@ h2 = torch.empty(3 * N, dtype=torch.float64).pin_memory()
 d = torch.empty(3 * N, dtype=torch.float64, device="cuda")
 d2 = torch.empty(3 * N, dtype=torch.float64, device="cuda")
 s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-for nch in (8, 32, 64):
-    bounds = [N * k // nch for k in range(nch + 1)]
+import numpy as np
+def ramp(nch, r):
+    # chunk weights: the first and last chunks r times smaller than the middle ones
+    w = np.ones(nch); w[0] = w[-1] = 1.0 / r
+    if nch > 4: w[1] = w[-2] = 2.0 / r
+    c = np.concatenate([[0], np.cumsum(w)]) / w.sum()
+    return [int(N * x) for x in c]
+for nch, r in ((32, 1), (64, 1), (32, 4), (64, 4), (32, 8), (48, 8)):
+    bounds = ramp(nch, r)
     def run():
         evs = []
         for k in range(nch):
@@ -33,5 +40,5 @@ for nch in (8, 32, 64):
         torch.cuda.synchronize()
     run()
     t = time.perf_counter(); run(); dt = time.perf_counter() - t
-    print(nch, "chunks:", round(dt * 1e3, 1), "ms ->", round(3 * N * 8 / dt / 1e9, 1), "GB/s per direction,",
+    print(nch, "chunks, ramp", r, ":", round(dt * 1e3, 1), "ms ->", round(3 * N * 8 / dt / 1e9, 1), "GB/s per direction,",
           round(683465475 / dt / 1e9, 3), "GDoF/s equivalent")
