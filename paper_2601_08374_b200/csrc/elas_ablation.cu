@@ -28,8 +28,24 @@ namespace elas {
 namespace abl {
 
 constexpr int NTE = 256;   // element-wise kernels
-// threads of the one-CTA-per-element kernels: 512 where an element's stage has >= 4096 fibres
-template <int N, int QQ> struct Ntc { static constexpr int value = 9 * QQ * QQ * N >= 4096 ? 512 : 256; };
+// threads of the one-CTA-per-element kernels: 512 where stage X has >= 512 fibres (9 q^2)
+template <int N, int QQ> struct Ntc { static constexpr int value = 9 * QQ * QQ >= 512 ? 512 : 256; };
+// elements per CTA: at p <= 5 enough stage-Y fibres (3 q n each) for the threads, within ~200 KB
+// of shared memory (config 4: p2 23.1 -> 18.9 ms, p4 10.9 -> 9.7); one at p >= 6, where two would
+// halve the resident threads
+template <int N, int QQ, int PE>
+struct Eba {
+  static constexpr int want = N <= 6 ? Ntc<N, QQ>::value / (3 * QQ * N) : 1;
+  static constexpr int cap = (200 * 1024 / 8) / PE;
+  static constexpr int w1 = want < 1 ? 1 : (want > 8 ? 8 : want);
+  static constexpr int value = w1 < cap ? w1 : (cap < 1 ? 1 : cap);
+};
+template <int N, int QQ> struct PeG {   // gradient kernel: Z1 | u / Y1 per element
+  static constexpr int value = 6 * QQ * N * N + (3 * N * N * N > 9 * QQ * QQ * N ? 3 * N * N * N : 9 * QQ * QQ * N);
+};
+template <int N, int QQ> struct PeD {   // transposed kernel: F | T1 | T2 per element
+  static constexpr int value = 9 * QQ * QQ * QQ + 9 * QQ * QQ * N + 6 * QQ * N * N;
+};
 
 __host__ __device__ inline int64_t grid_of(int64_t n, int nt) {
   const int64_t g = (n + nt - 1) / nt;
@@ -209,50 +225,88 @@ __global__ void point_kernel(const double* __restrict__ qd, const double* __rest
 //   Y1[c][d][a3][a2][i] = sum_j (d == 1 ? D : B)[a2][j] Z1[c][d == 2][a3][j][i]
 //   G[c][d](a1, a2, a3) = sum_i (d == 0 ? D : B)[a1][i] Y1[c][d][a3][a2][i]   -> Q[e][pt][3c + d]
 template <int N, int QQ>
-__global__ void __launch_bounds__(Ntc<N, QQ>::value) grad_sf_kernel(const double* __restrict__ E, const double* __restrict__ tab,
-                                                      double* __restrict__ Q, int64_t e0) {
+__global__ void __launch_bounds__(Ntc<N, QQ>::value, 1) grad_sf_kernel(const double* __restrict__ E, const double* __restrict__ tab,
+                                                      double* __restrict__ Q, int64_t e0, int64_t e1) {
   extern __shared__ double sm[];
   constexpr int n = N, q = QQ, n2 = n * n, n3 = n2 * n, q2 = q * q, q3 = q2 * q, NTC = Ntc<N, QQ>::value;
+  constexpr int PE = PeG<N, QQ>::value, EB = Eba<N, QQ, PE>::value;
   double* B = sm;
   double* D = B + q * n;
-  double* Z1 = D + q * n;         // 3 * 2 * q * n^2
-  double* u = Z1 + 6 * q * n2;    // 3 n^3, dead after stage Z ...
-  double* Y1 = u;                 // ... so stage Y writes over it (3 * 3 * q^2 * n)
-  const int64_t e = e0 + blockIdx.x;
+  // per element el: Z1 = D + q n + el PE (3 * 2 * q * n^2), then u (3 n^3, dead after stage Z, so
+  // stage Y writes Y1 = 3 * 3 * q^2 * n over it)
+#define ABL_Z1(el) (D + q * n + (el) * PE)
+#define ABL_U(el) (ABL_Z1(el) + 6 * q * n2)
+  const int64_t eb = e0 + (int64_t)blockIdx.x * EB;
+  const int ne = (int)((e1 - eb) < EB ? (e1 - eb) : EB);
   for (int t = threadIdx.x; t < 2 * q * n; t += NTC) sm[t] = tab[t];
-  for (int t = threadIdx.x; t < 3 * n3; t += NTC) u[t] = E[e * 3 * n3 + t];
+  for (int t = threadIdx.x; t < ne * 3 * n3; t += NTC) ABL_U(t / (3 * n3))[t % (3 * n3)] = E[eb * 3 * n3 + t];
   __syncthreads();
-  for (int t = threadIdx.x; t < 6 * q * n2; t += NTC) {
-    const int ji = t % n2, a3 = (t / n2) % q, zk = (t / (n2 * q)) % 2, c = t / (2 * q * n2);
-    const double* T = zk ? D : B;
-    double acc = 0.0;
+  // one thread per 1D fibre, its n (or q) inputs loaded once into registers
+  for (int t = threadIdx.x; t < ne * 3 * n2; t += NTC) {            // stage Z: fibre (c, j, i)
+    const int el = t / (3 * n2), ji = t % n2, c = (t / n2) % 3;
+    const double* u = ABL_U(el);
+    double* Z1 = ABL_Z1(el);
+    double v[n];
 #pragma unroll
-    for (int k = 0; k < n; ++k) acc = fma(T[a3 * n + k], u[c * n3 + k * n2 + ji], acc);
-    Z1[t] = acc;
+    for (int k = 0; k < n; ++k) v[k] = u[c * n3 + k * n2 + ji];
+#pragma unroll 1   // coefficients reloaded per output (hoisting them all spills)
+    for (int a3 = 0; a3 < q; ++a3) {
+      double sb = 0.0, sd = 0.0;
+#pragma unroll
+      for (int k = 0; k < n; ++k) {
+        sb = fma(B[a3 * n + k], v[k], sb);
+        sd = fma(D[a3 * n + k], v[k], sd);
+      }
+      Z1[((c * 2 + 0) * q + a3) * n2 + ji] = sb;
+      Z1[((c * 2 + 1) * q + a3) * n2 + ji] = sd;
+    }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < 9 * q2 * n; t += NTC) {
-    const int i = t % n, a2 = (t / n) % q, a3 = (t / (n * q)) % q, d = (t / (n * q2)) % 3, c = t / (3 * n * q2);
-    const double* T = d == 1 ? D : B;
-    const double* z = Z1 + ((c * 2 + (d == 2)) * q + a3) * n2 + i;
-    double acc = 0.0;
+  for (int t = threadIdx.x; t < ne * 3 * q * n; t += NTC) {         // stage Y: fibre (c, a3, i)
+    const int el = t / (3 * q * n), i = t % n, a3 = (t / n) % q, c = (t / (n * q)) % 3;
+    const double* Z1 = ABL_Z1(el);
+    double* Y1 = ABL_U(el);
+    double vb[n], vd[n];
 #pragma unroll
-    for (int j = 0; j < n; ++j) acc = fma(T[a2 * n + j], z[j * n], acc);
-    Y1[t] = acc;
+    for (int j = 0; j < n; ++j) {
+      vb[j] = Z1[((c * 2 + 0) * q + a3) * n2 + j * n + i];
+      vd[j] = Z1[((c * 2 + 1) * q + a3) * n2 + j * n + i];
+    }
+#pragma unroll 1   // coefficients reloaded per output (hoisting them all spills)
+    for (int a2 = 0; a2 < q; ++a2) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < n; ++j) {
+        s0 = fma(B[a2 * n + j], vb[j], s0);
+        s1 = fma(D[a2 * n + j], vb[j], s1);
+        s2 = fma(B[a2 * n + j], vd[j], s2);
+      }
+      Y1[(((c * 3 + 0) * q + a3) * q + a2) * n + i] = s0;
+      Y1[(((c * 3 + 1) * q + a3) * q + a2) * n + i] = s1;
+      Y1[(((c * 3 + 2) * q + a3) * q + a2) * n + i] = s2;
+    }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < 9 * q3; t += NTC) {
-    const int cd = t % 9, pt = t / 9;
-    const int c = cd / 3, d = cd % 3;
-    const int a1 = pt % q, a2 = (pt / q) % q, a3 = pt / q2;
-    const double* T = d == 0 ? D : B;
-    const double* yv = Y1 + (((c * 3 + d) * q + a3) * q + a2) * n;
-    double acc = 0.0;
+  for (int t = threadIdx.x; t < ne * 9 * q2; t += NTC) {            // stage X: fibre (c, d, a3, a2)
+    const int el = t / (9 * q2), a2 = t % q, a3 = (t / q) % q, cd = (t / q2) % 9;
+    const int64_t e = eb + el;
+    const double* Y1 = ABL_U(el);
+    const double* T = (cd % 3) == 0 ? D : B;
+    double v[n];
 #pragma unroll
-    for (int i = 0; i < n; ++i) acc = fma(T[a1 * n + i], yv[i], acc);
-    Q[(e * q3 + pt) * 9 + cd] = acc;
+    for (int i = 0; i < n; ++i) v[i] = Y1[((cd * q + a3) * q + a2) * n + i];
+#pragma unroll 1   // coefficients reloaded per output (hoisting them all spills)
+    for (int a1 = 0; a1 < q; ++a1) {
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < n; ++i) acc = fma(T[a1 * n + i], v[i], acc);
+      Q[(e * q3 + a1 + q * (a2 + q * a3)) * 9 + cd] = acc;
+    }
   }
 }
+
+#undef ABL_Z1
+#undef ABL_U
 
 // stages 1-2: transposed sum factorisation (Alg. 1 Kernel 2 with C1), one CTA per element.
 // voigt = 1: Q holds the 6 stress components; F = sigma~ A~^T is formed on load from qdata.
@@ -260,20 +314,26 @@ __global__ void __launch_bounds__(Ntc<N, QQ>::value) grad_sf_kernel(const double
 //   T2[c][zk][a3][j][i] = zk = 0: sum_a2 B[a2][j] T1[c][0] + D[a2][j] T1[c][1];  zk = 1: sum_a2 B[a2][j] T1[c][2]
 //   Eo[c][k][j][i]      = sum_a3 B[a3][k] T2[c][0] + D[a3][k] T2[c][1]
 template <int N, int QQ>
-__global__ void __launch_bounds__(Ntc<N, QQ>::value) div_sf_kernel(const double* __restrict__ Q, const double* __restrict__ qd,
+__global__ void __launch_bounds__(Ntc<N, QQ>::value, 1) div_sf_kernel(const double* __restrict__ Q, const double* __restrict__ qd,
                                                      const double* __restrict__ tab, double* __restrict__ Eo, int voigt,
-                                                     int64_t e0) {
+                                                     int64_t e0, int64_t e1) {
   extern __shared__ double sm[];
   constexpr int n = N, q = QQ, n2 = n * n, n3 = n2 * n, q2 = q * q, q3 = q2 * q, NTC = Ntc<N, QQ>::value;
+  constexpr int PE = PeD<N, QQ>::value, EB = Eba<N, QQ, PE>::value;
   double* B = sm;
   double* D = B + q * n;
-  double* F = D + q * n;          // [c][d][pt], 9 q^3
-  double* T1 = F + 9 * q3;        // 9 q^2 n
-  double* T2 = T1 + 9 * q2 * n;   // 6 q n^2
-  const int64_t e = e0 + blockIdx.x;
+  // per element el: F ([c][d][pt], 9 q^3) | T1 (9 q^2 n) | T2 (6 q n^2)
+#define ABL_F(el) (D + q * n + (el) * PE)
+#define ABL_T1(el) (ABL_F(el) + 9 * q3)
+#define ABL_T2(el) (ABL_T1(el) + 9 * q2 * n)
+  const int64_t eb = e0 + (int64_t)blockIdx.x * EB;
+  const int ne = (int)((e1 - eb) < EB ? (e1 - eb) : EB);
   for (int t = threadIdx.x; t < 2 * q * n; t += NTC) sm[t] = tab[t];
   if (voigt) {
-    for (int pt = threadIdx.x; pt < q3; pt += NTC) {
+    for (int t = threadIdx.x; t < ne * q3; t += NTC) {
+      const int el = t / q3, pt = t % q3;
+      const int64_t e = eb + el;
+      double* F = ABL_F(el);
       const double* sv = Q + (e * q3 + pt) * 9;
       const double S[3][3] = {{sv[0], sv[5], sv[4]}, {sv[5], sv[1], sv[3]}, {sv[4], sv[3], sv[2]}};
       double A[9];
@@ -283,54 +343,81 @@ __global__ void __launch_bounds__(Ntc<N, QQ>::value) div_sf_kernel(const double*
           F[(c * 3 + d) * q3 + pt] = fma(S[c][2], A[3 * d + 2], fma(S[c][1], A[3 * d + 1], S[c][0] * A[3 * d]));
     }
   } else {
-    for (int t = threadIdx.x; t < 9 * q3; t += NTC) {
-      const int cd = t % 9, pt = t / 9;
-      F[cd * q3 + pt] = Q[e * q3 * 9 + t];
+    for (int t = threadIdx.x; t < ne * 9 * q3; t += NTC) {
+      const int el = t / (9 * q3), cd = t % 9, pt = (t / 9) % q3;
+      ABL_F(el)[cd * q3 + pt] = Q[eb * q3 * 9 + t];
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < 9 * q2 * n; t += NTC) {
-    const int i = t % n, a2 = (t / n) % q, a3 = (t / (n * q)) % q, cd = t / (n * q2);
+  for (int t = threadIdx.x; t < ne * 9 * q2; t += NTC) {            // stage Xt: fibre (c, d, a3, a2)
+    const int el = t / (9 * q2), a2 = t % q, a3 = (t / q) % q, cd = (t / q2) % 9;
+    const double* F = ABL_F(el);
+    double* T1 = ABL_T1(el);
     const double* T = (cd % 3) == 0 ? D : B;
-    const double* f = F + cd * q3 + (a3 * q + a2) * q;
-    double acc = 0.0;
+    double v[q];
 #pragma unroll
-    for (int a1 = 0; a1 < q; ++a1) acc = fma(T[a1 * n + i], f[a1], acc);
-    T1[t] = acc;
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < 6 * q * n2; t += NTC) {
-    const int i = t % n, j = (t / n) % n, a3 = (t / n2) % q, zk = (t / (n2 * q)) % 2, c = t / (2 * q * n2);
-    double acc = 0.0;
-    if (zk == 0) {
-      const double* t0 = T1 + ((c * 3 + 0) * q + a3) * q * n + i;
-      const double* t1 = T1 + ((c * 3 + 1) * q + a3) * q * n + i;
+    for (int a1 = 0; a1 < q; ++a1) v[a1] = F[cd * q3 + (a3 * q + a2) * q + a1];
+#pragma unroll 1   // coefficients reloaded per output (hoisting them all spills)
+    for (int i = 0; i < n; ++i) {
+      double acc = 0.0;
 #pragma unroll
-      for (int a2 = 0; a2 < q; ++a2) acc = fma(B[a2 * n + j], t0[a2 * n], fma(D[a2 * n + j], t1[a2 * n], acc));
-    } else {
-      const double* t2 = T1 + ((c * 3 + 2) * q + a3) * q * n + i;
-#pragma unroll
-      for (int a2 = 0; a2 < q; ++a2) acc = fma(B[a2 * n + j], t2[a2 * n], acc);
+      for (int a1 = 0; a1 < q; ++a1) acc = fma(T[a1 * n + i], v[a1], acc);
+      T1[((cd * q + a3) * q + a2) * n + i] = acc;
     }
-    T2[t] = acc;
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < 3 * n3; t += NTC) {
-    const int ji = t % n2, k = (t / n2) % n, c = t / n3;
-    const double* tb = T2 + (c * 2 + 0) * q * n2 + ji;
-    const double* td = T2 + (c * 2 + 1) * q * n2 + ji;
-    double acc = 0.0;
+  for (int t = threadIdx.x; t < ne * 3 * q * n; t += NTC) {         // stage Yt: fibre (c, a3, i)
+    const int el = t / (3 * q * n), i = t % n, a3 = (t / n) % q, c = (t / (n * q)) % 3;
+    const double* T1 = ABL_T1(el);
+    double* T2 = ABL_T2(el);
+    double v0[q], v1[q], v2[q];
 #pragma unroll
-    for (int a3 = 0; a3 < q; ++a3) acc = fma(B[a3 * n + k], tb[a3 * n2], fma(D[a3 * n + k], td[a3 * n2], acc));
-    Eo[e * 3 * n3 + t] = acc;
+    for (int a2 = 0; a2 < q; ++a2) {
+      v0[a2] = T1[(((c * 3 + 0) * q + a3) * q + a2) * n + i];
+      v1[a2] = T1[(((c * 3 + 1) * q + a3) * q + a2) * n + i];
+      v2[a2] = T1[(((c * 3 + 2) * q + a3) * q + a2) * n + i];
+    }
+#pragma unroll 1   // coefficients reloaded per output (hoisting them all spills)
+    for (int j = 0; j < n; ++j) {
+      double sb = 0.0, sd = 0.0;
+#pragma unroll
+      for (int a2 = 0; a2 < q; ++a2) {
+        sb = fma(B[a2 * n + j], v0[a2], fma(D[a2 * n + j], v1[a2], sb));
+        sd = fma(B[a2 * n + j], v2[a2], sd);
+      }
+      T2[((c * 2 + 0) * q + a3) * n2 + j * n + i] = sb;
+      T2[((c * 2 + 1) * q + a3) * n2 + j * n + i] = sd;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < ne * 3 * n2; t += NTC) {            // stage Zt: fibre (c, j, i)
+    const int el = t / (3 * n2), ji = t % n2, c = (t / n2) % 3;
+    const int64_t e = eb + el;
+    const double* T2 = ABL_T2(el);
+    double vb[q], vd[q];
+#pragma unroll
+    for (int a3 = 0; a3 < q; ++a3) {
+      vb[a3] = T2[((c * 2 + 0) * q + a3) * n2 + ji];
+      vd[a3] = T2[((c * 2 + 1) * q + a3) * n2 + ji];
+    }
+#pragma unroll 1   // coefficients reloaded per output (hoisting them all spills)
+    for (int k = 0; k < n; ++k) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a3 = 0; a3 < q; ++a3) acc = fma(B[a3 * n + k], vb[a3], fma(D[a3 * n + k], vd[a3], acc));
+      Eo[e * 3 * n3 + c * n3 + k * n2 + ji] = acc;
+    }
   }
 }
 
-size_t grad_sf_smem(int n, int q) {
-  const int un = 3 * n * n * n > 9 * q * q * n ? 3 * n * n * n : 9 * q * q * n;   // u and Y1 share
-  return sizeof(double) * (2 * q * n + 6 * q * n * n + un);
-}
-size_t div_sf_smem(int n, int q) { return sizeof(double) * (2 * q * n + 9 * q * q * q + 9 * q * q * n + 6 * q * n * n); }
+#undef ABL_F
+#undef ABL_T1
+#undef ABL_T2
+
+template <int N, int QQ>
+size_t grad_sf_smem() { return sizeof(double) * (2 * QQ * N + (size_t)Eba<N, QQ, PeG<N, QQ>::value>::value * PeG<N, QQ>::value); }
+template <int N, int QQ>
+size_t div_sf_smem() { return sizeof(double) * (2 * QQ * N + (size_t)Eba<N, QQ, PeD<N, QQ>::value>::value * PeD<N, QQ>::value); }
 
 template <int N, int QQ>
 cudaError_t run_stage(const elas_op* op, int stage, const double* x, double* y, int64_t e0, int64_t e1, cudaStream_t st,
@@ -346,14 +433,19 @@ cudaError_t run_stage(const elas_op* op, int stage, const double* x, double* y, 
   gather_kernel<N><<<(unsigned)grid_of(nel * 3 * n3, NTE), NTE, 0, st>>>(s, x, op->abl_E, e0, e1);
   if (stage == 0)
     grad_dense_kernel<N, QQ><<<(unsigned)grid_of(nel * q3, NTE), NTE, 0, st>>>(op->abl_E, op->abl_G, op->abl_Q, e0, e1);
-  else
-    grad_sf_kernel<N, QQ><<<(unsigned)nel, Ntc<N, QQ>::value, grad_sf_smem(N, QQ), st>>>(op->abl_E, op->tab, op->abl_Q, e0);
+  else {
+    constexpr int EB = Eba<N, QQ, PeG<N, QQ>::value>::value;
+    grad_sf_kernel<N, QQ><<<(unsigned)((nel + EB - 1) / EB), Ntc<N, QQ>::value, grad_sf_smem<N, QQ>(), st>>>(
+        op->abl_E, op->tab, op->abl_Q, e0, e1);
+  }
   point_kernel<QQ><<<(unsigned)grid_of(nel * q3, NTE), NTE, 0, st>>>(op->qd, op->rr, op->abl_Q, stage >= 2, e0, e1);
   if (stage == 0)
     div_dense_kernel<N, QQ><<<(unsigned)grid_of(nel * 3 * n3, NTE), NTE, 0, st>>>(op->abl_Q, op->abl_G, op->abl_Eo, e0, e1);
-  else
-    div_sf_kernel<N, QQ><<<(unsigned)nel, Ntc<N, QQ>::value, div_sf_smem(N, QQ), st>>>(op->abl_Q, op->qd, op->tab, op->abl_Eo,
-                                                                         stage >= 2, e0);
+  else {
+    constexpr int EB = Eba<N, QQ, PeD<N, QQ>::value>::value;
+    div_sf_kernel<N, QQ><<<(unsigned)((nel + EB - 1) / EB), Ntc<N, QQ>::value, div_sf_smem<N, QQ>(), st>>>(
+        op->abl_Q, op->qd, op->tab, op->abl_Eo, stage >= 2, e0, e1);
+  }
   scatter_kernel<N><<<(unsigned)grid_of(nel * 3 * n3, NTE), NTE, 0, st>>>(s, op->abl_Eo, y, e0, e1);
   return cudaGetLastError();
 }
