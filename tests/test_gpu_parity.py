@@ -612,7 +612,7 @@ def test_anisotropic_isotropic_voigt_equals_isotropic_op():
     assert rel_l2(ya, yi) <= 1e-13
 
 
-@pytest.mark.parametrize("faces,variant", [(0, 0), (63, 0), (1 | 8 | 16, 4), (63, 3), (2 | 32, 2)])
+@pytest.mark.parametrize("faces,variant", [(0, 0), (63, 0), (1 | 8 | 16, 4), (63, 3), (2 | 32, 2), (1 | 16, 8), (63, 9)])
 def test_apply_add_accumulates(faces, variant):
     """elas_apply_add: y += A x with identity rows counted once on edges/corners of several faces."""
     torch = torch_mod()
