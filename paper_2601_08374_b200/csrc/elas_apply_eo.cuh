@@ -88,8 +88,12 @@ template <> struct MinbEO<8> { static constexpr int value = ELAS_EO_MINB_P8; };
 #define ELAS_EO32_MINB_LO 0
 #endif
 template <int P> struct MinbEO32 {
-  static constexpr int value = P == 7 ? 4 : P == 8 ? 3 : P == 5 ? 2 : (ELAS_EO32_MINB_LO > 0 ? ELAS_EO32_MINB_LO : MinbEO<P>::value);
+  static constexpr int value = P == 7 ? 4 : P == 8 ? 3 : P == 5 ? 2 : P == 6 ? 4
+                               : (ELAS_EO32_MINB_LO > 0 ? ELAS_EO32_MINB_LO : MinbEO<P>::value);
 };
+// CTA size per precision: the FP32 p = 6 instance runs one element per 64-thread CTA, 4 CTAs/SM
+// (measured, config 4: 52.7 -> 53.4 GDoF/s; the FP64 instance loses, 33.6 -> 33.3)
+template <int P, typename T> struct NtEOT { static constexpr int value = (sizeof(T) == 4 && P == 6) ? 64 : NtEO<P>::value; };
 
 // Persistent CTAs (measured, config 4): a win only where ONE CTA fills an SM (p = 5: 256 threads,
 // 167 KB smem) and nothing else covers a CTA's start-up latency: 28.4 -> 30.1 GDoF/s; elsewhere
@@ -103,7 +107,7 @@ template <int P> struct PersistEO { static constexpr bool value = ELAS_EO_PERSIS
 #define ELAS_EO_NOPAD_P 0   // a degree whose tiles go unpadded (experiment knob; 0 = none)
 #endif
 template <int P, int Q, typename T = double>
-using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEO<P>::value, (int)sizeof(T), P == ELAS_EO_NOPAD_P ? 0 : 1>;
+using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEOT<P, T>::value, (int)sizeof(T), P == ELAS_EO_NOPAD_P ? 0 : 1>;
 
 // Quadrature-data ring (ELAS_QD_RING = R > 0): every stage-X thread owns one x-line (EB q^2 <=
 // NT), so it streams ITS line's 9 values per point into its own shared-memory slots with
