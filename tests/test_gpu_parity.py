@@ -680,3 +680,23 @@ def test_pipelined_zeroing_chunk_planes(p, dims, faces):
     Z = oracle.constrained_mask(m)
     assert np.array_equal(y[Z], P.x[Z])
     assert np.all(np.abs(y) < 1e100)
+
+
+@pytest.mark.parametrize("p,variant", [(1, 6), (2, 6), (8, 6), (2, 5), (8, 5)])
+def test_config4_full_size_otf_and_f32(p, variant):
+    """Full-size config 4 for the geometry-on-the-fly (6; p = 1 runs the thread-per-element
+    kernel) and mixed-precision (5) operators: sampled rows vs the oracle at each contract."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_config(4, p)
+    op = Operator.from_problem(P, variant=variant)
+    assert op.variant == variant
+    x = torch.from_numpy(P.x).cuda()
+    y = torch.empty_like(x)
+    op.apply(x, y)
+    torch.cuda.synchronize()
+    op.close()
+    yh = y.cpu().numpy()
+    rows = sample_rows(P, 160, 70 + p, extra=plane_rows(P, P.p * 3, 16, p))
+    y_ref = oracle.apply_rows(oracle_mesh(P), P.x, rows)
+    assert rel_l2(yh[rows], y_ref) <= (TOL_F32 if variant == 5 else TOL)
