@@ -700,3 +700,23 @@ def test_config4_full_size_otf_and_f32(p, variant):
     rows = sample_rows(P, 160, 70 + p, extra=plane_rows(P, P.p * 3, 16, p))
     y_ref = oracle.apply_rows(oracle_mesh(P), P.x, rows)
     assert rel_l2(yh[rows], y_ref) <= (TOL_F32 if variant == 5 else TOL)
+
+
+@pytest.mark.parametrize("p", [2, 6])
+def test_anisotropic_config4_sampled(p):
+    """Full-size config 4 with a random SPD Voigt matrix per element (the bench's anisotropic
+    row): sampled rows vs the oracle."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_config(4, p)
+    C6 = synth.random_C6(np.random.default_rng(90 + p), (P.nz, P.ny, P.nx))
+    lam, mu = P.material_arrays()
+    m = oracle.Mesh(P.vertex_array(), P.p, P.q, lam, mu, P.dirichlet_faces, C6=C6)
+    op = Operator.anisotropic(P, C6)
+    x = torch.from_numpy(P.x).cuda()
+    y = torch.empty_like(x)
+    op.apply(x, y)
+    torch.cuda.synchronize()
+    op.close()
+    rows = sample_rows(P, 160, 80 + p, extra=plane_rows(P, P.p * 3, 16, p))
+    assert rel_l2(y.cpu().numpy()[rows], oracle.apply_rows(m, P.x, rows)) <= TOL
