@@ -76,3 +76,24 @@ def test_ablation_no_deterministic_mode_and_host_apply():
     y_ref = _oracle_y(P)
     assert np.linalg.norm(yh.numpy() - y_ref) <= TOL * np.linalg.norm(y_ref)
     op.close()
+
+
+@pytest.mark.parametrize("variant", STAGES)
+def test_ablation_stage_config4_p8_sampled(variant):
+    """The bench's ablation workload (config 4, p = 8, 50.9M DoF): sampled rows vs the oracle."""
+    torch = _torch()
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_config(4, 8)
+    op = Operator.from_problem(P, variant=variant)
+    x = torch.from_numpy(P.x).cuda()
+    y = torch.empty_like(x)
+    op.apply(x, y)
+    torch.cuda.synchronize()
+    op.close()
+    rng = np.random.default_rng(variant)
+    rows = np.unique(rng.choice(P.num_dofs, size=128, replace=False))
+    lam, mu = P.material_arrays()
+    m = oracle.Mesh(P.vertex_array(), P.p, P.q, lam, mu, P.dirichlet_faces)
+    y_ref = oracle.apply_rows(m, P.x, rows)
+    yh = y.cpu().numpy()[rows]
+    assert np.linalg.norm(yh - y_ref) <= TOL * np.linalg.norm(y_ref)
