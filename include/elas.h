@@ -271,8 +271,12 @@ int elas_dot(elas_op* op, const double* a, const double* b, double* result);
  *   Coarsest level: PCG preconditioned by its Chebyshev smoother, to coarse_rtol (> 0:
  *   synchronising convergence test) or exactly coarse_maxit iterations (coarse_rtol <= 0: no
  *   host round trip).  Host arrays are copied.  NULL + message on error.
+ * create needs levels >= 2 (ELAS_EINVAL-style NULL otherwise).
  * apply: one V-cycle x = M b (x overwritten; pre- and post-smoothing with the same Chebyshev
- *   polynomial, so M is symmetric).  DEVICE b, x of the finest level's length; asynchronous.
+ *   polynomial).  M is a fixed symmetric linear map only when the coarse solve converges to
+ *   coarse_rtol > 0; with the default fixed-length coarse PCG (coarse_rtol <= 0) M depends on b
+ *   (nonlinear), and elas_pcg_gmg then uses the flexible-CG (Polak-Ribiere) beta.  DEVICE b, x
+ *   of the finest level's length; asynchronous.
  * level_op: the op of level l (0 = finest), owned by the gmg (do not destroy).
  * pcg_gmg: elas_pcg with the V-cycle as preconditioner (op: typically elas_gmg_level_op(g, 0)). */
 typedef struct elas_gmg elas_gmg;

@@ -424,9 +424,10 @@ cudaError_t run_stage(const elas_op* op, int stage, const double* x, double* y, 
                       bool first) {
   constexpr int n3 = N * N * N, q3 = QQ * QQ * QQ;
   cudaError_t err;
-  if (first &&
-      ((err = cudaFuncSetAttribute(grad_sf_kernel<N, QQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) ||
-       (err = cudaFuncSetAttribute(div_sf_kernel<N, QQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024))))
+  (void)first;
+  // per-device function attributes: set on the current device on every call (not a hot path)
+  if ((err = cudaFuncSetAttribute(grad_sf_kernel<N, QQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) ||
+      (err = cudaFuncSetAttribute(div_sf_kernel<N, QQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)))
     return err;
   const Slab& s = op->slab;
   const int64_t nel = e1 - e0;
@@ -470,13 +471,19 @@ cudaError_t ablation_apply(elas_op* op, int stage, const double* x, double* y, i
   const int p = op->p, q = op->q, n = p + 1, n3 = n * n * n, q3 = q * q * q;
   const int64_t ne = (int64_t)s.nx * s.ny * s.nz;
   cudaError_t err;
-  const bool first = !op->abl_E;
+  const bool first = !(op->abl_E && op->abl_Eo && op->abl_Q && op->abl_G);
   if (first) {
     if ((err = cudaMalloc(&op->abl_E, sizeof(double) * 3 * n3 * ne)) ||
         (err = cudaMalloc(&op->abl_Eo, sizeof(double) * 3 * n3 * ne)) ||
         (err = cudaMalloc(&op->abl_Q, sizeof(double) * 9 * (size_t)q3 * ne)) ||
-        (err = cudaMalloc(&op->abl_G, sizeof(double) * (size_t)q3 * 3 * n3)))
+        (err = cudaMalloc(&op->abl_G, sizeof(double) * (size_t)q3 * 3 * n3))) {
+      // all or nothing: a later call must not find part of the scratch and skip the allocation
+      for (double** b : {&op->abl_E, &op->abl_Eo, &op->abl_Q, &op->abl_G}) {
+        if (*b) cudaFree(*b);
+        *b = nullptr;
+      }
       return err;
+    }
     gm_kernel<<<(unsigned)grid_of((int64_t)q3 * 3 * n3, NTE), NTE, 0, st>>>(n, q, op->tab, op->abl_G);
     if ((err = cudaGetLastError())) return err;
   }

@@ -27,16 +27,6 @@ static constexpr bool kAutoThread = ELAS_AUTO_THREAD != 0;
 #define ELAS_AUTO_FOLDED 1
 #endif
 static constexpr bool kAutoFolded = ELAS_AUTO_FOLDED != 0;
-#ifndef ELAS_INIT_CHUNKS
-// z-chunks of the pipelined y zeroing in elas_apply (1 = off, the default).  Measured and
-// rejected: 8 chunks 33.5 -> 33.3 GDoF/s at config 5, p2 18.5 -> 17.8, p4 27.5 -> 25.8 at config 4
-// (16 chunks worse): the high-priority memset CTAs and their HBM writes slow the apply more than
-// the 0.75 ms memset they hide, and every chunk boundary drains the apply grid.
-#define ELAS_INIT_CHUNKS 1
-#endif
-#ifndef ELAS_INIT_CHUNK_MIN_ELEMS
-#define ELAS_INIT_CHUNK_MIN_ELEMS (1 << 18)   // below this the whole memset is a few microseconds
-#endif
 #ifndef ELAS_HOST_CHUNKS
 #define ELAS_HOST_CHUNKS 64   // z-chunks of the pipelined host apply
 #endif
@@ -169,12 +159,10 @@ void free_op(elas_op* op) {
   if (op->ev_comm) cudaEventDestroy(op->ev_comm);
   for (cudaEvent_t ev : op->prof_ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : op->host_ev) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : op->init_ev) cudaEventDestroy(ev);
   cudaFree(op->abl_E);
   cudaFree(op->abl_Eo);
   cudaFree(op->abl_Q);
   cudaFree(op->abl_G);
-  if (op->init_stream) cudaStreamDestroy(op->init_stream);
   if (op->h2d) cudaStreamDestroy(op->h2d);
   if (op->d2h) cudaStreamDestroy(op->d2h);
   elas::free_solver_state(op);
@@ -617,23 +605,11 @@ static int range_launches(const elas_op* op, int z0, int z1) {
   return n;
 }
 
-// Number of z-chunks the single-op apply pipelines its y zeroing over (1 = one memset up front).
-static int init_chunks(const elas_op* op) {
-  const Slab& s = op->slab;
-  const int64_t ne = (int64_t)s.nx * s.ny * s.nz;
-  if (!(op->nranks == 1 || op->external) || op->deterministic || ELAS_INIT_CHUNKS < 2 ||
-      ne < ELAS_INIT_CHUNK_MIN_ELEMS || s.nz < 2 * ELAS_INIT_CHUNKS)
-    return 1;
-  return ELAS_INIT_CHUNKS;
-}
-
 int elas_launches_per_apply(const elas_op* op) {
   if (!op) return -1;
   // init = a memset (not a kernel) + the Dirichlet-face copy kernel when faces are constrained
   int n = op->slab.faces ? 1 : 0;
   const int nzl = op->ez1 - op->ez0;
-  const int nch = init_chunks(op);
-  if (nch > 1) return n + nch;   // one apply launch per z-chunk (memsets are not kernels)
   if (op->nranks == 1 || op->external) return n + range_launches(op, 0, nzl);
   const bool lo = op->rank > 0, hi = op->rank < op->nranks - 1;
   int i0 = 0, i1 = nzl;
@@ -645,58 +621,12 @@ int elas_launches_per_apply(const elas_op* op) {
   return n;
 }
 
-// y = A x with the zeroing of y pipelined under the apply: chunk k = element
-// layers [z_k, z_k+1) owns node planes [z_k p, z_k+1 p) (the last chunk also the top plane).  Its
-// apply adds into planes [z_k p, z_k+1 p], so it waits for the zeroing of chunks k and k+1; the
-// zeroing of chunk k+2 runs on a high-priority side stream while chunk k computes (HBM is not the
-// apply's limiter).  Constrained rows are copied from x once at the end (the apply never writes
-// them).  Only the first two chunks' memsets are exposed instead of all of y's.
-static int pipelined_apply(elas_op* op, const double* x, double* y, int nch) {
-  const Slab& s = op->slab;
-  cudaStream_t st = op->stream;
-  if (!op->init_stream) {
-    int lo = 0, hi = 0;
-    CUDA_OR(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
-    CUDA_OR(cudaStreamCreateWithPriority(&op->init_stream, cudaStreamNonBlocking, hi), "cudaStreamCreate");
-  }
-  while ((int)op->init_ev.size() < nch + 1) {
-    cudaEvent_t ev;
-    CUDA_OR(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
-    op->init_ev.push_back(ev);
-  }
-  const int64_t layer = (int64_t)s.nx * s.ny;
-  const int p = op->p;
-  auto zb = [&](int k) { return (int)(((int64_t)k * s.nz) / nch); };
-  auto planes = [&](int k, int& K0, int& K1) { K0 = zb(k) * p; K1 = k == nch - 1 ? s.Nz : zb(k + 1) * p; };
-  Slab s0 = s;
-  s0.faces = 0;   // zero only: the constrained rows are set from x after the last chunk
-  int K0, K1;
-  // the side stream must not zero y before earlier work on the op's stream is done with it
-  CUDA_OR(cudaEventRecord(op->init_ev[nch], st), "cudaEventRecord");
-  CUDA_OR(cudaStreamWaitEvent(op->init_stream, op->init_ev[nch], 0), "cudaStreamWaitEvent");
-  for (int k = 0; k < nch; ++k) {
-    planes(k, K0, K1);
-    cudaStream_t zs = k < 2 ? st : op->init_stream;
-    CUDA_OR(elas::launch_init_planes(s0, K0, K1, x, y, zs), "y zeroing");
-    if (k >= 2) CUDA_OR(cudaEventRecord(op->init_ev[k], zs), "cudaEventRecord");
-  }
-  int rc;
-  for (int k = 0; k < nch; ++k) {
-    if (k + 1 < nch && k + 1 >= 2) CUDA_OR(cudaStreamWaitEvent(st, op->init_ev[k + 1], 0), "cudaStreamWaitEvent");
-    if ((rc = range_apply(op, x, y, zb(k) * layer, zb(k + 1) * layer, st))) return rc;
-  }
-  CUDA_OR(elas::launch_face_copy(s, x, y, st), "face copy launch");
-  return ELAS_OK;
-}
-
 int elas_apply(elas_op* op, const double* x, double* y) {
   if (!op || !x || !y) { set_error("elas_apply: NULL argument"); return ELAS_EINVAL; }
   if (x == y) { set_error("elas_apply: x and y must not alias"); return ELAS_EINVAL; }
   if (((uintptr_t)x | (uintptr_t)y) & 7u) { set_error("elas_apply: x, y must be 8-byte aligned"); return ELAS_EINVAL; }
   const Slab& s = op->slab;
   cudaStream_t st = op->stream;
-  const int nch = init_chunks(op);
-  if (nch > 1) return pipelined_apply(op, x, y, nch);
   CUDA_OR(elas::launch_init(s, x, y, st), "init kernel launch");
   const int64_t layer = (int64_t)s.nx * s.ny;
   const int64_t ne = layer * s.nz;

@@ -507,24 +507,13 @@ cudaError_t launch_apply_pq(const Slab& s, const double* x, double* y, const dou
                             const double* rr, const double* tables, int64_t e_begin, int64_t e_end,
                             cudaStream_t st) {
   using C = Cfg<P, Q>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t err = cudaFuncSetAttribute(apply_kernel<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)C::smem);
-    if (err != cudaSuccess) return err;
-    attr_done = true;
-  }
+  static KernelPrep prep;   // per device
+  int pref = 0;
+  cudaError_t err = prep.prep(apply_kernel<P, Q>, C::NT, C::smem, &pref);
+  if (err != cudaSuccess) return err;
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
   const int64_t grid = (ne + C::EB - 1) / C::EB;
-  static int pref = -1;
-  if (pref < 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_kernel<P, Q>, C::NT, C::smem);
-    pref = sms * (per_sm > 0 ? per_sm : 1);
-  }
   apply_kernel<P, Q><<<(unsigned)grid, C::NT, C::smem, st>>>(x, y, qd, rr, tables, s, e_begin, e_end, pref);
   return cudaGetLastError();
 }

@@ -98,16 +98,10 @@ template <int P, typename T> struct NtEOT { static constexpr int value = (sizeof
 // Persistent CTAs (measured, config 4): a win only where ONE CTA fills an SM (p = 5: 256 threads,
 // 167 KB smem) and nothing else covers a CTA's start-up latency: 28.4 -> 30.1 GDoF/s; elsewhere
 // the second resident CTA already does and the loop costs registers (p6 33.4 -> 32.3).
-#ifndef ELAS_EO_PERSIST
-#define ELAS_EO_PERSIST 0
-#endif
-template <int P> struct PersistEO { static constexpr bool value = ELAS_EO_PERSIST != 0 || P == 5; };
+template <int P> struct PersistEO { static constexpr bool value = P == 5; };
 
-#ifndef ELAS_EO_NOPAD_P
-#define ELAS_EO_NOPAD_P 0   // a degree whose tiles go unpadded (experiment knob; 0 = none)
-#endif
 template <int P, int Q, typename T = double>
-using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEOT<P, T>::value, (int)sizeof(T), P == ELAS_EO_NOPAD_P ? 0 : 1>;
+using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEOT<P, T>::value, (int)sizeof(T), 1>;
 
 // Quadrature-data ring (ELAS_QD_RING = R > 0): every stage-X thread owns one x-line (EB q^2 <=
 // NT), so it streams ITS line's 9 values per point into its own shared-memory slots with
@@ -122,26 +116,15 @@ using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEOT<P, T>::value, (int)sizeof(T), 
 #endif
 // whole-CTA TMA staging of qdata where two CTAs fit (elas_apply.cuh); off at p = 2, which
 // runs faster at 4 CTAs/SM without it (12.5 -> 16 GDoF/s)
-#ifndef ELAS_EO_NOSTAGE_P3
-#define ELAS_EO_NOSTAGE_P3 1   // measured: p = 3 without staging at 3 CTAs/SM 21.4 -> 22.2
-#endif
-template <int P> struct StageEO { static constexpr bool value = P != 2 && !(P == 3 && ELAS_EO_NOSTAGE_P3); };
-#ifndef ELAS_QD_L1PF
-#define ELAS_QD_L1PF 0
-#endif
-#ifndef ELAS_X_PREFETCH
-#define ELAS_X_PREFETCH 0
-#endif
-#ifndef ELAS_QD_RING_ALIAS
-#define ELAS_QD_RING_ALIAS 1
-#endif
+// measured: p = 3 without staging at 3 CTAs/SM 21.4 -> 22.2
+template <int P> struct StageEO { static constexpr bool value = P != 2 && P != 3; };
 template <int P, int Q, typename T = double>
 struct RingEO {
   using C = CfgEO<P, Q, T>;
   static constexpr int WB = (int)sizeof(T);
-  // ALIAS: the ring lives in the Z buffer, idle during stage X (first copies issued after the
-  // stage-Y barrier); otherwise it gets its own shared memory and starts at CTA begin.
-  static constexpr bool ALIAS = ELAS_QD_RING_ALIAS != 0;
+  // the ring lives in the Z buffer, idle during stage X (first copies issued after the stage-Y
+  // barrier); a dedicated ring costs occupancy and lost everywhere
+  static constexpr bool ALIAS = true;
   static constexpr int RMAX = ALIAS ? (C::EB * C::ZE) / (9 * C::NT) : 16;
   static constexpr int R0 = ELAS_QD_RING < RMAX ? ELAS_QD_RING : RMAX;
   static constexpr int R = R0 >= 2 ? R0 : 0;
@@ -353,7 +336,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + C::BASE + EB * C::QDE);
 
   const int tid = threadIdx.x;
-  // PST (persistent CTAs, ELAS_EO_PERSIST): the grid covers the resident CTAs and each walks the
+  // PST (persistent CTAs, p = 5): the grid covers the resident CTAs and each walks the
   // batches b, b + gridDim.x, ...; the next batch's z-columns are gathered into registers right
   // after the stage-Yt barrier so the loads fly during stage Zt, and the tables load once.
   constexpr bool PST = PersistEO<P>::value && !COLORED && !OTF && !ANISO;
@@ -471,22 +454,6 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
       const uintptr_t a1 = a0 + (uintptr_t)(pne * C::QDE * sizeof(T));
       const uintptr_t lo = a0 & ~(uintptr_t)15, hi = (a1 + 15) & ~(uintptr_t)15;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
-    }
-  }
-#endif
-#if ELAS_X_PREFETCH
-  // the z-column this thread will gather in the CTA one wave ahead, pulled into L2 now
-  if (!COLORED && pref_ctas > 0) {
-    const int64_t pe = e0 + (int64_t)pref_ctas * EB + zel;
-    if (zel < EB && tid < EB * N * N && pe < e_end) {
-      int pex, pey, pez;
-      elem_coords<false>(cm, s, pe, pex, pey, pez);
-      const int64_t pbase = (pex * P + zi) + (int64_t)s.Nx * (pey * P + zj) + plane * ((int64_t)pez * P);
-#pragma unroll
-      for (int k = 0; k < N; ++k)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(x + c * s.nodes + pbase + k * plane));
     }
   }
 #endif
@@ -727,13 +694,6 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
 #pragma unroll
           for (int f = 0; f < 9; ++f) An[f] = qp[((a1 + 1) * 9 + f) * Q * Q];
         }
-#if ELAS_QD_L1PF > 0
-        if (!STG && a1 + 1 + ELAS_QD_L1PF < Q) {   // L1 prefetch further ahead (no registers)
-#pragma unroll
-          for (int f = 0; f < 9; ++f)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(qp + ((a1 + 1 + ELAS_QD_L1PF) * 9 + f) * Q * Q));
-        }
-#endif
       }
       T G[3][3];
 #pragma unroll
@@ -945,19 +905,10 @@ cudaError_t launch_apply_eo_pqc(const Slab& s, const double* x, double* y, const
                                 const ColorMap& cm, const double* cc = nullptr) {
   using C = CfgEO<P, Q, T>;
   constexpr size_t SMEM = OTF ? OtfSmem<P, Q, T>::smem : ANISO ? AnisoSmem<P, Q, T>::smem : RingEO<P, Q, T>::smem;
-  static bool attr_done = false;
-  static int pref = -1;
-  if (!attr_done) {
-    cudaError_t err = cudaFuncSetAttribute(apply_eo_kernel<P, Q, T, COLORED, OTF, ANISO>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    if (err != cudaSuccess) return err;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_eo_kernel<P, Q, T, COLORED, OTF, ANISO>, C::NT, SMEM);
-    pref = sms * (per_sm > 0 ? per_sm : 1);
-    attr_done = true;
-  }
+  static KernelPrep prep;   // per device: the shared-memory attribute and the resident-CTA count
+  int pref = 0;
+  cudaError_t err = prep.prep(apply_eo_kernel<P, Q, T, COLORED, OTF, ANISO>, C::NT, SMEM, &pref);
+  if (err != cudaSuccess) return err;
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
   const int64_t nb = (ne + C::EB - 1) / C::EB;

@@ -237,14 +237,10 @@ __global__ void __launch_bounds__(NT, ELAS_P1T_MINB)
 template <int Q, bool OTF>
 cudaError_t launch_q(const Slab& s, const double* x, double* y, const double* qd, const double* rr,
                      const double* tables, int64_t e_begin, int64_t e_end, cudaStream_t st, const double* gauss) {
-  static int pref = -1;
-  if (pref < 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_p1_kernel<Q, OTF>, NT, 0);
-    pref = sms * (per_sm > 0 ? per_sm : 1);
-  }
+  static KernelPrep prep;   // per device
+  int pref = 0;
+  cudaError_t e = prep.prep(apply_p1_kernel<Q, OTF>, NT, 0, &pref);
+  if (e != cudaSuccess) return e;
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
   const int64_t grid = (ne + NT - 1) / NT;

@@ -14,19 +14,10 @@ cudaError_t apply_tc_launch(const Slab& s, const double* x, double* y, const dou
                             const double* tables, int64_t e_begin, int64_t e_end, cudaStream_t st) {
   ApplyLaunch L;
   apply_tc_info(&L);
-  static bool attr = false;
-  static int pref = 0;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::apply_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)L.smem_bytes);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc::apply_tc_kernel, L.threads, L.smem_bytes);
-    pref = sms * (per_sm > 0 ? per_sm : 1);
-    attr = true;
-  }
+  static KernelPrep prep;   // per device
+  int pref = 0;
+  cudaError_t e = prep.prep(tc::apply_tc_kernel, L.threads, L.smem_bytes, &pref);
+  if (e != cudaSuccess) return e;
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
   const int64_t grid = (ne + tc::EPC - 1) / tc::EPC;

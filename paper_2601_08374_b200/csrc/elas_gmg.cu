@@ -271,7 +271,9 @@ elas_gmg* elas_gmg_create(const elas_mesh* fine, int p, int q, const double* lam
                           double coarse_rtol, int coarse_maxit, int variant) {
   using elas::set_error;
   if (!fine || !lambda || !mu) { set_error("elas_gmg_create: NULL argument"); return nullptr; }
-  if (levels < 1 || coarse_maxit < 1) { set_error("elas_gmg_create: need levels >= 1 and coarse_maxit >= 1"); return nullptr; }
+  // levels >= 2: with one level the coarse solve would run on the finest op and share its PCG
+  // work vectors and scalar slots with the outer elas_pcg_gmg iteration
+  if (levels < 2 || coarse_maxit < 1) { set_error("elas_gmg_create: need levels >= 2 and coarse_maxit >= 1"); return nullptr; }
   const int f = 1 << (levels - 1);
   if (fine->nranks > 1 && fine->nz % (fine->nranks * f)) {
     set_error("elas_gmg_create: z-slabs need nz divisible by nranks * 2^(levels-1) (aligned slabs on every level)");
@@ -427,8 +429,9 @@ int elas_pcg_gmg(elas_op* op, elas_gmg* g, const double* b, double* x, double rt
     return ELAS_EINVAL;
   }
   if (b == x || maxit < 0 || !(rtol >= 0.0)) { elas::set_error("elas_pcg_gmg: need b != x, maxit >= 0, rtol >= 0"); return ELAS_EINVAL; }
+  // flexible CG unless the coarse solve converges to a tolerance (then M is a fixed linear map)
   return elas::pcg_core(op, elas::PC_CALLBACK, [g](const double* r, double* z) { return elas::vcycle_graph(g, r, z); }, b,
-                        x, rtol, maxit, true, rep, history);
+                        x, rtol, maxit, true, rep, history, !(g->coarse_rtol > 0.0));
 }
 
 void elas_gmg_destroy(elas_gmg* g) {

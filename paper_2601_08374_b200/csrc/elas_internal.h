@@ -1,6 +1,7 @@
 // Internal declarations shared by the libelas translation units.
 #pragma once
 #include <cstdint>
+#include <mutex>
 #include <string>
 
 #include <cuda_runtime.h>
@@ -109,5 +110,37 @@ cudaError_t launch_plane_add(const Slab& s, int which_plane, double* y, const do
 
 // error helpers
 void set_error(const std::string& msg);
+
+// Per-device, thread-safe one-time launch preparation of a kernel: the dynamic shared-memory
+// attribute (a per-device function attribute) and the resident-CTA count of the grid
+// (SMs x CTAs per SM at this CTA size and shared memory).  One static KernelPrep per kernel
+// instance; every launch calls prep() on the current device.
+constexpr int kMaxDevices = 64;
+struct KernelPrep {
+  std::mutex m;
+  bool done[kMaxDevices] = {};
+  int resident[kMaxDevices] = {};
+  template <typename K>
+  cudaError_t prep(K kern, int threads, size_t smem, int* resident_ctas) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> g(m);
+    if (!done[dev]) {
+      if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+      }
+      int sms = 0, per_sm = 0;
+      if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem)) != cudaSuccess) return e;
+      resident[dev] = sms * (per_sm > 0 ? per_sm : 1);
+      done[dev] = true;
+    }
+    if (resident_ctas) *resident_ctas = resident[dev];
+    return cudaSuccess;
+  }
+};
 
 }  // namespace elas

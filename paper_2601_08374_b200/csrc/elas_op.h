@@ -26,8 +26,6 @@ struct elas_op {
   cudaStream_t h2d = nullptr, d2h = nullptr;   // copy streams of the chunked host apply
   std::vector<cudaEvent_t> host_ev;            // per chunk: x landed, chunk computed
   double *abl_E = nullptr, *abl_Eo = nullptr, *abl_Q = nullptr, *abl_G = nullptr;   // ablation-stage scratch
-  cudaStream_t init_stream = nullptr;          // pipelined y zeroing of elas_apply (high priority)
-  std::vector<cudaEvent_t> init_ev;            // per z-chunk: its node planes zeroed
   cudaStream_t stream = nullptr;
   // multi-GPU
   ncclComm_t comm = nullptr;
@@ -65,8 +63,10 @@ constexpr int PC_CALLBACK = 100;
 int cheb_run(elas_cheb* ch, const double* b, double* x, bool x_zero);
 // PCG from x = 0; kind: ELAS_PC_NONE / ELAS_PC_JACOBI / PC_CALLBACK (M).  check = false: exactly
 // maxit iterations with no host synchronisation (a fixed-length inner solve).
+// flexible: Polak-Ribiere beta (flexible CG) for a preconditioner that is not a fixed linear map
+// (the V-cycle with a fixed-length inner PCG coarse solve)
 int pcg_core(elas_op* op, int kind, const PrecondFn& M, const double* b, double* x, double rtol, int maxit,
-             bool check, elas_solve_report* rep, double* history);
+             bool check, elas_solve_report* rep, double* history, bool flexible = false);
 // exchange the partial interface planes of y with the neighbour ranks and add them (NCCL mode,
 // synchronous on the op's stream); no-op for nranks == 1 or external mode
 int exchange_planes(elas_op* op, double* y);

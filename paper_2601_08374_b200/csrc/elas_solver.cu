@@ -28,7 +28,7 @@ namespace {
 constexpr int RED_BLOCKS = 296;    // 2 x 148 SMs; fixed so the reduction order is fixed
 constexpr int RED_THREADS = 256;
 // device scalar slots after the RED_BLOCKS partials
-enum { S_DOT = 0, S_RZ, S_RZNEW, S_PT, S_NRM, S_LAM, S_COUNT };
+enum { S_DOT = 0, S_RZ, S_RZNEW, S_PT, S_NRM, S_LAM, S_ZT, S_COUNT };
 
 int fail(cudaError_t e, const char* what) {
   set_error(std::string(what) + ": " + cudaGetErrorString(e));
@@ -347,10 +347,14 @@ __global__ void pcg_update_kernel(double* __restrict__ x, double* __restrict__ r
   }
 }
 
-// PCG: beta = S[RZNEW] / S[RZ]; p = z + beta p; then S[RZ] = S[RZNEW] (one thread, after use)
+// PCG: beta = S[RZNEW] / S[RZ] (Fletcher-Reeves), or with a variable preconditioner (flexible CG,
+// Polak-Ribiere form) beta = z_new.(r_new - r_old) / rz_old = -(z_new.t) / (p.t), using
+// r_old = r_new + alpha t and alpha = rz_old / (p.t); p = z + beta p; then S[RZ] = S[RZNEW]
 __global__ void pcg_direction_kernel(double* __restrict__ p, const double* __restrict__ z, double* __restrict__ S,
-                                     int64_t n, int first) {
-  const double beta = (first || S[S_RZ] == 0.0) ? 0.0 : S[S_RZNEW] / S[S_RZ];
+                                     int64_t n, int first, int flexible) {
+  const double beta = first ? 0.0
+                      : flexible ? (S[S_PT] != 0.0 ? -S[S_ZT] / S[S_PT] : 0.0)
+                                 : (S[S_RZ] == 0.0 ? 0.0 : S[S_RZNEW] / S[S_RZ]);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
     p[t] = first ? z[t] : fma(beta, p[t], z[t]);
 }
@@ -409,11 +413,8 @@ int diag_raw(elas_op* op, double* d) {
   const Slab& s = op->slab;
   const int p = op->p, q = op->q, n = p + 1;
   const size_t smem = sizeof(double) * (size_t)(5 * q * n + 3 * (q * q * q + q * q * n + q * n * n + n * n * n));
-  static size_t attr = 0;
-  if (smem > attr) {
-    CK(cudaFuncSetAttribute(diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "cudaFuncSetAttribute");
-    attr = smem;
-  }
+  // a per-device function attribute: set on the op's (current) device on every call (setup path)
+  CK(cudaFuncSetAttribute(diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "cudaFuncSetAttribute");
   diag_init_kernel<<<grid_for(3 * s.nodes), 256, 0, op->stream>>>(s, d);
   const int64_t ne = (int64_t)s.nx * s.ny * s.nz;
   const double* gauss = op->tab + tables_gauss_offset(p, q, fold_table_size(p, q));
@@ -478,7 +479,7 @@ int cheb_run(elas_cheb* ch, const double* b, double* x, bool x_zero) {
 }
 
 int pcg_core(elas_op* op, int kind, const PrecondFn& M, const double* b, double* x, double rtol, int maxit,
-             bool check, elas_solve_report* rep, double* history) {
+             bool check, elas_solve_report* rep, double* history, bool flexible) {
   int rc;
   if ((rc = ensure_red(op))) return rc;
   if (kind == ELAS_PC_JACOBI && (rc = ensure_dinv(op))) return rc;
@@ -513,7 +514,7 @@ int pcg_core(elas_op* op, int kind, const PrecondFn& M, const double* b, double*
   double rel = rz0 > 0.0 ? 1.0 : 0.0;
   if (history) history[0] = rel;
   if (rz0 > 0.0) {
-    pcg_direction_kernel<<<g, 256, 0, st>>>(p, z, S, n, 1);
+    pcg_direction_kernel<<<g, 256, 0, st>>>(p, z, S, n, 1, 0);
     while (it < maxit) {
       if ((rc = elas_apply(op, p, t))) return rc;
       if ((rc = dot(op, p, t, S_PT))) return rc;
@@ -522,6 +523,7 @@ int pcg_core(elas_op* op, int kind, const PrecondFn& M, const double* b, double*
       CK(cudaGetLastError(), "pcg update kernel");
       if (!fused_z && (rc = M(r, z))) return rc;
       if ((rc = dot(op, r, z, S_RZNEW))) return rc;
+      if (flexible && (rc = dot(op, z, t, S_ZT))) return rc;
       ++it;
       if (check) {
         double rz = 0.0;
@@ -530,7 +532,7 @@ int pcg_core(elas_op* op, int kind, const PrecondFn& M, const double* b, double*
         if (history) history[it] = rel;
         if (rel <= rtol) break;
       }
-      pcg_direction_kernel<<<g, 256, 0, st>>>(p, z, S, n, 0);
+      pcg_direction_kernel<<<g, 256, 0, st>>>(p, z, S, n, 0, flexible ? 1 : 0);
       copy_scalar_kernel<<<1, 1, 0, st>>>(S, S_RZ, S_RZNEW);
       CK(cudaGetLastError(), "pcg direction kernels");
     }

@@ -10,6 +10,7 @@ import pytest
 
 import oracle
 import synth
+from tests import oracle_pool
 
 pytestmark = pytest.mark.gpu
 
@@ -121,14 +122,16 @@ def test_config2_full():
 
 
 def test_config3_sampled_rows():
+    """>= 4096 seeded random rows + rows on the Dirichlet face x = 0 and on an
+    element-boundary plane."""
     P = synth.make_config(3)
     Nx, Ny, Nz = P.node_dims
     N = Nx * Ny * Nz
-    # random rows + rows on the Dirichlet face x=0 + rows on element-boundary planes
     face = np.arange(0, N, Nx)[:50]
-    rows = sample_rows(P, 384, 0, extra=np.concatenate([face, N + face, plane_rows(P, 6, 40, 1)]))
+    rows = sample_rows(P, 4096, 0, extra=np.concatenate([face, N + face, plane_rows(P, 6, 40, 1)]))
+    assert rows.size >= 4096
     y = gpu_apply(P)
-    y_ref = oracle.apply_rows(oracle_mesh(P), P.x, rows)
+    y_ref = oracle_pool.apply_rows(oracle_mesh(P), P.x, rows)
     assert rel_l2(y[rows], y_ref) <= TOL
     Z = oracle.constrained_mask(oracle_mesh(P))
     assert np.array_equal(y[Z], P.x[Z])             # identity rows, bitwise
@@ -147,8 +150,9 @@ def test_config4_full_size(p):
     op.apply(x, y)
     torch.cuda.synchronize()
     yh = y.cpu().numpy()
-    rows = sample_rows(P, 160 if p >= 7 else 256, p, extra=plane_rows(P, P.p * 3, 16, p))
-    y_ref = oracle.apply_rows(oracle_mesh(P), P.x, rows)
+    rows = sample_rows(P, 4096, p, extra=plane_rows(P, P.p * 3, 16, p))
+    assert rows.size >= 4096
+    y_ref = oracle_pool.apply_rows(oracle_mesh(P), P.x, rows)
     assert rel_l2(yh[rows], y_ref) <= TOL
     # rigid modes at full size: translation and the rotation (-y, x, 0) of the affine grid
     Nx, Ny, Nz = P.node_dims
@@ -176,18 +180,38 @@ def test_config4_full_size(p):
 
 
 def test_config5_full_size_sampled():
-    """Config 5 (683M dofs) on one GPU: sampled rows incl. every slab-interface plane of the
-    2/4/8-GPU partitions."""
+    """Config 5 (683M dofs) on one GPU in the bench's launch configuration: >= 4096 seeded random
+    rows, EVERY row of the 2-GPU interface plane and sampled rows of the other 4/8-GPU
+    interface planes; then the host-buffer apply (elas_apply_host, the bench's
+    e2e call, 64 z-chunks) equal to the device apply."""
+    torch = torch_mod()
+    from paper_2601_08374_b200.elas import Operator
     P = synth.make_config(5)
     p = P.p
-    extra = []
-    for nr in (2, 4, 8):
+    Nx, Ny, Nz = P.node_dims
+    N = Nx * Ny * Nz
+    K2 = (P.nz // 2) * p                                   # the P = 2 interface plane
+    full_plane = np.concatenate([c * N + K2 * Nx * Ny + np.arange(Nx * Ny) for c in range(3)])
+    extra = [full_plane]
+    for nr in (4, 8):
         for r in range(1, nr):
-            extra.append(plane_rows(P, (r * P.nz // nr) * p, 8, 10 * nr + r))
-    rows = sample_rows(P, 256, 5, extra=np.concatenate(extra))
-    y = gpu_apply(P)
-    y_ref = oracle.apply_rows(oracle_mesh(P), P.x, rows)
+            K = (r * P.nz // nr) * p
+            if K != K2:
+                extra.append(plane_rows(P, K, 64, 10 * nr + r))
+    rows = sample_rows(P, 4096, 5, extra=np.concatenate(extra))
+    assert rows.size >= 4096 + full_plane.size
+    op = Operator.from_problem(P)
+    y = gpu_apply(P, op=op)
+    y_ref = oracle_pool.apply_rows(oracle_mesh(P), P.x, rows)
     assert rel_l2(y[rows], y_ref) <= TOL
+    assert rel_l2(y[full_plane], y_ref[np.searchsorted(rows, full_plane)]) <= TOL
+    # elas_apply_host at the bench's schedule (ELAS_HOST_CHUNKS = 64 z-chunks)
+    xh = torch.from_numpy(P.x).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    op.apply_host(xh, yh)
+    op.close()
+    assert rel_l2(yh.numpy(), y) <= 1e-15
+    del xh, yh
 
 
 # ---------------------------------------------------------------------------------------
@@ -255,14 +279,25 @@ def test_error_paths_on_gpu():
     op.close()
 
 
+_LOOPBACK_REF = {}
+
+
+def loopback_problem():
+    P = synth.make_problem("t", 5, 4, 16, 6, 8, perturb=True, lognormal_material=True,
+                           faces=1 | 16 | 32, seed=33)
+    if "y" not in _LOOPBACK_REF:                      # one oracle apply for all partitions
+        _LOOPBACK_REF["y"] = oracle.apply(oracle_mesh(P), P.x)
+    return P, _LOOPBACK_REF["y"]
+
+
 @pytest.mark.parametrize("nranks", [2, 3, 4, 8])
 def test_slab_loopback_external_exchange(nranks):
     """P slab operators on ONE GPU in external-exchange mode, interface planes summed with the
-    library's own plane-add kernel: equals the single-GPU apply to 1e-14 relative."""
+    library's own plane-add kernel (the A6 interface sum, PAPER.md:169 P^T): equals the oracle's
+    apply to 1e-12 and the single-GPU apply to 1e-14 relative."""
     torch = torch_mod()
     from paper_2601_08374_b200.elas import Operator
-    P = synth.make_problem("t", 5, 4, 16, 6, 8, perturb=True, lognormal_material=True,
-                           faces=1 | 16 | 32, seed=33)
+    P, y_ref = loopback_problem()
     y_full = gpu_apply(P)
     Nx, Ny, Nz = P.node_dims
     plane = Nx * Ny
@@ -298,6 +333,7 @@ def test_slab_loopback_external_exchange(nranks):
     for op in ops:
         op.close()
     assert rel_l2(yg.reshape(-1), y_full) <= 1e-14
+    assert rel_l2(yg.reshape(-1), y_ref) <= TOL
 
 
 # ---------------------------------------------------------------------------------------
@@ -504,6 +540,7 @@ def test_deterministic_config4_and_slabs():
         yg[:, ks[r][0]:ks[r][1] + 1] = ys[r].view(3, -1, plane).cpu().numpy()
         ops[r].close()
     assert rel_l2(yg.reshape(-1), y_full) <= 1e-14
+    assert rel_l2(yg.reshape(-1), oracle.apply(oracle_mesh(P), P.x)) <= TOL   # the A6 sum vs the oracle
 
 
 def test_deterministic_only_folded():

@@ -112,3 +112,13 @@ def test_gmg_slab_alignment_rejected_before_any_device_work():
         elas.elas_gmg_create(2, 2, 12, 2, 4, 1.0, 1.0, levels=3, rank=0, nranks=2)   # 12 % 8 != 0
     with pytest.raises(elas.ElasError, match="divisible"):
         elas.elas_gmg_create(2, 3, 8, 2, 4, 1.0, 1.0, levels=2)                       # ny odd
+
+
+def test_gmg_rejects_single_level():
+    """elas_gmg_create needs levels >= 2: with one level the coarse PCG would run on the finest
+    op and share its work vectors with the outer elas_pcg_gmg.  The argument check
+    precedes every CUDA call, so this runs without a GPU."""
+    from paper_2601_08374_b200 import elas
+    lam = np.ones(8)
+    with pytest.raises(elas.ElasError, match="levels >= 2"):
+        elas.elas_gmg_create(2, 2, 2, 2, 4, lam, lam, levels=1)
