@@ -150,6 +150,34 @@ def blas_threads():
     return os.cpu_count()
 
 
+def cpu_info():
+    """CPU model, physical cores and logical CPUs of this host (lscpu; /proc/cpuinfo fallback)."""
+    info = {"cpu_model": None, "physical_cores": None, "logical_cpus": os.cpu_count()}
+    try:
+        import subprocess
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for ln in out.splitlines():
+            if ":" in ln:
+                k, v = ln.split(":", 1)
+                kv[k.strip()] = v.strip()
+        info["cpu_model"] = kv.get("Model name")
+        if kv.get("Core(s) per socket") and kv.get("Socket(s)"):
+            info["physical_cores"] = int(kv["Core(s) per socket"]) * int(kv["Socket(s)"])
+    except Exception:
+        pass
+    if info["cpu_model"] is None:
+        try:
+            with open("/proc/cpuinfo") as f:
+                for ln in f:
+                    if ln.startswith("model name"):
+                        info["cpu_model"] = ln.split(":", 1)[1].strip()
+                        break
+        except Exception:
+            pass
+    return info
+
+
 def cpu_baseline(P, budget_s=12.0):
     nel = 4
     t, ne, desc = oracle_time(P, nel)
@@ -157,7 +185,7 @@ def cpu_baseline(P, budget_s=12.0):
         nel = int(ne * max(2.0, min(8.0, budget_s / max(t, 1e-3) / 2)))
         t, ne, desc = oracle_time(P, nel)
     value = P.num_dofs * (ne / P.num_elements) / t / 1e9
-    return {"value": value, "unit": "GDoF/s", "cores": blas_threads(), "kind": "oracle",
+    return {"value": value, "unit": "GDoF/s", "cores": blas_threads(), "kind": "oracle", **cpu_info(),
             "sample": f"{desc} ({ne} elements, {t:.1f} s; extrapolated to {P.num_elements} elements)"}
 
 
@@ -619,7 +647,9 @@ def run_ours(args):
     hbm_peak = peaks.get("hbm_gbs")
     roof = {"bound": "alu", "achieved": round(F / tk / 1e12, 3), "peak": round(PEAK_FP64_DERIVED / 1e12, 2),
             "unit": "TFLOP/s", "frac": round(F / tk / PEAK_FP64_DERIVED, 4), "traffic": None,
-            "peak_kind": "derived FP64 DFMA pipe: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md 6)",
+            "peak_kind": ("derived FP64 pipe: 148 SM x 64 FMA/clk x 2 flop x 1.965 GHz = 37.2 TF/s (MEASURED_PEAKS.json "
+                          "has no FP64 entry); measured on this pool's B200: DMMA 37.1 TF/s, all-register DFMA "
+                          "34.1 TF/s (tools/microbench/dmma_rates.cu, fp64_probe.cu; DESIGN.md 6)"),
             "alg_flops_per_apply": F, "alg_bytes_per_apply": B,
             "hbm_achieved_gbs": round(B / tk / 1e9, 1),
             "hbm_frac_of_measured": round(B / tk / 1e9 / hbm_peak, 4) if hbm_peak else None,
@@ -701,6 +731,7 @@ def run_reference(args):
             "config": {"workload": workload_desc(P), "dofs": P.num_dofs, "elements": P.num_elements,
                        "p": P.p, "q": P.q},
             "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": blas_threads(), "kind": "oracle",
+                             **cpu_info(),
                              "sample": f"each step: {desc}, extrapolated to {P.num_elements} elements"},
             "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
