@@ -99,6 +99,14 @@ template <int P, typename T> struct NtEOT { static constexpr int value = (sizeof
 // 167 KB smem) and nothing else covers a CTA's start-up latency: 28.4 -> 30.1 GDoF/s; elsewhere
 // the second resident CTA already does and the loop costs registers (p6 33.4 -> 32.3).
 template <int P> struct PersistEO { static constexpr bool value = P == 5; };
+// Stage-Z gather with 32-bit word offsets (3 nodes < 2^31 per rank, checked by elas_create) and the
+// L2::256B prefetch hint on the loads; measured (config 4, GDoF/s): p4 27.4 -> 28.4, p5 30.1 ->
+// 30.5, p7 23.8 -> 24.3, p8 30.4 -> 30.7, but p6 33.5 -> 32.6 (its 255-register budget spills).
+// Measured and rejected: waiting on the qdata ring per PAIR of points (p6 33.5 -> 33.0, p7 -5 %).
+#ifndef ELAS_EO_G32_MASK
+#define ELAS_EO_G32_MASK 0x1BC   // degrees (bit p) with the 32-bit gather: 2, 3, 4, 5, 7, 8
+#endif
+template <int P> struct G32EO { static constexpr bool value = ((ELAS_EO_G32_MASK >> P) & 1) != 0; };
 
 template <int P, int Q, typename T = double>
 using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEOT<P, T>::value, (int)sizeof(T), 1>;
@@ -357,12 +365,34 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
       int ex, ey, ez;
       elem_coords<COLORED>(cm, s, g0 + zel, ex, ey, ez);
       const int I = ex * P + zi, J = ey * P + zj;
+      if constexpr (G32EO<P>::value) {
+      // 32-bit word offsets; loads carry the L2::256B prefetch hint
+      const uint32_t nodes32 = (uint32_t)s.nodes, plane32 = (uint32_t)plane;
+      const double* xb = x + ((uint32_t)I + (uint32_t)s.Nx * (uint32_t)J + plane32 * (uint32_t)(ez * P));
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double v;
+          asm("ld.global.nc.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(xb + (c * nodes32 + k * plane32)));
+          u[c][k] = (T)v;
+        }
+      if (bc) {
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+          if (is_constrained(I, J, ez * P + k, s)) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) u[c][k] = T(0);
+          }
+      }
+      } else {
       const int64_t base = I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         const bool cons = bc && is_constrained(I, J, ez * P + k, s);
 #pragma unroll
         for (int c = 0; c < 3; ++c) u[c][k] = cons ? T(0) : (T)__ldg(x + c * s.nodes + base + k * plane);
+      }
       }
     }
   };

@@ -20,9 +20,9 @@ cudaError_t apply_tc_launch(const Slab& s, const double* x, double* y, const dou
   if (e != cudaSuccess) return e;
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
-  const int64_t grid = (ne + tc::EPC - 1) / tc::EPC;
-  tc::apply_tc_kernel<<<(unsigned)grid, L.threads, L.smem_bytes, st>>>(x, y, qd, rr, tables, s, e_begin, e_end,
-                                                                      pref);
+  const int64_t nb = (ne + tc::EPC - 1) / tc::EPC;
+  const int64_t grid = nb < pref ? nb : pref;   // persistent element slots
+  tc::apply_tc_kernel<<<(unsigned)grid, L.threads, L.smem_bytes, st>>>(x, y, qd, rr, tables, s, e_begin, e_end);
   return cudaGetLastError();
 }
 

@@ -17,6 +17,18 @@
 //   A 16x4: a0 = A[g][t], a1 = A[g+8][t];  B 4x8: b0 = B[t][g];
 //   C 16x8: c0 = C[g][2t], c1 = C[g][2t+1], c2 = C[g+8][2t], c3 = C[g+8][2t+1].
 //
+// Even-odd folding where one input feeds two tables (GLL/Gauss symmetry, elas_apply_eo.cuh):
+// XF contracts u+ = u_i + u_{6-i} and u- = u_i - u_{6-i} (K = 4 node pairs) against the folded
+// [B | D] tables in one E and one O MMA (2 instead of 4 per tile), and YF does the same for the
+// two y-contractions of UX0 (w1 = Dy UX0, w2 = By UX0: 2 instead of 4 MMAs per component);
+// out_a = E + O, out_{7-a} = +-(E - O).  The single-table contractions (ZF, ZB, YB, XB, w0)
+// gain nothing from folding on the tensor path and stay plain.
+//
+// Persistent element slots: the grid covers the SMs, each slot (WPE warps) walks the elements
+// e0 + el, e0 + el + EPC gridDim, ... with its own named barrier, and at the start of each
+// element pulls the NEXT element's x rows and quadrature data into L2 (prefetch.global.L2 and
+// one cp.async.bulk.prefetch.L2), so the global loads of the next XF and slices hit L2.
+//
 // Per element (e):
 //   XF  fibres (c,j,k), K=i      : UX[c][0] = Bx u, UX[c][1] = Dx u          (global x -> smem UX)
 //   for each a1-slice s (a1 = 2s, 2s+1):
@@ -42,16 +54,10 @@ constexpr int UX_J = 8, UX_K = N * UX_J, UX_V = N * UX_K, UX_C = 2 * UX_V, UX_SI
 // loads of the z stage cover 16 distinct banks.
 constexpr int U2_A = 8, U2_K = 2 * U2_A, U2_W = N * U2_K, U2_C = 3 * U2_W, U2_SIZE = 3 * U2_C;
 #ifndef ELAS_TC_EPC
-#define ELAS_TC_EPC 6
+#define ELAS_TC_EPC 4   // measured (config 4, p6): 4 -> 31.4, 5 -> 25.0, 6 -> 28.3 GDoF/s (6, 5: 168 regs + spills)
 #endif
 #ifndef ELAS_TC_WPE
 #define ELAS_TC_WPE 2
-#endif
-#ifndef ELAS_TC_PF
-#define ELAS_TC_PF 1
-#endif
-#ifndef ELAS_TC_AQ_EARLY
-#define ELAS_TC_AQ_EARLY 1
 #endif
 constexpr int EPC = ELAS_TC_EPC;               // elements per CTA
 constexpr int WPE = ELAS_TC_WPE;               // warps per element (2 or 4): slices split between them
@@ -60,6 +66,7 @@ constexpr int XTILES = (3 * N * N + 15) / 16;       // 10 fibre tiles in the x s
 constexpr int XT_PER_WARP = (XTILES + WPE - 1) / WPE;
 static_assert(NSLICE % WPE == 0, "slices must split evenly over the warps of an element");
 constexpr int QD_PER_ELEM = 9 * Q * Q * Q;     // 4608 doubles, fragment order (see qdata kernel)
+constexpr int FTS = 4 * N + 4 * Q;             // doubles per folded table (fold_table_size(6, 8))
 
 // swizzled offsets inside one (c, v) block of UX / one (c, w) block of U2
 __device__ __forceinline__ int uxo(int k, int j, int a1) {
@@ -129,34 +136,18 @@ __device__ __forceinline__ void fibre(int f, int& c, int& j, int& k) {
 __global__ void __launch_bounds__(32 * WPE * EPC, 1)
     apply_tc_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
                     const double* __restrict__ rr, const double* __restrict__ tables, Slab s,
-                    int64_t e_begin, int64_t e_end, int pref_ctas) {
+                    int64_t e_begin, int64_t e_end) {
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int el = warp / WPE, half = warp % WPE;   // `half`: this warp's index within its element
   const int g = lane >> 2, t = lane & 3;
-  const int64_t cta_e0 = e_begin + (int64_t)blockIdx.x * EPC;
-  const int64_t e = cta_e0 + el;
-#if ELAS_L2_PREFETCH
-  // TMA bulk prefetch of quadrature data into L2 (ELAS_TC_PF: 1 = the CTA one wave ahead,
-  // 2 = this CTA's own elements at CTA start, 3 = 2 + each warp's next slice)
-  if (threadIdx.x == 0 && pref_ctas > 0) {
-    const int64_t pe0 = (ELAS_TC_PF == 1) ? cta_e0 + (int64_t)pref_ctas * EPC : cta_e0;
-    if (pe0 < e_end) {
-      const int64_t pne = (e_end - pe0) < EPC ? (e_end - pe0) : EPC;
-      const uintptr_t a0 = (uintptr_t)(qd + pe0 * (int64_t)QD_PER_ELEM);
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0),
-                   "r"((uint32_t)(pne * QD_PER_ELEM * 8)) : "memory");
-    }
-  }
-#endif
-  if (e >= e_end) return;  // both warps of an element exit together
   double* UX = smem + el * ELEM_SMEM;
   double* U2 = UX + UX_SIZE + half * U2_SIZE;
 
-  // coefficient fragments (registers, whole kernel).  tables = B[a][i] (Q x N) then D.
+  // coefficient fragments (registers, whole kernel).  tables = B[a][i] (Q x N), D, fold(B), fold(D)
   const double* TB = tables;
   const double* TD = tables + Q * N;
-  double FB[2], FD[2], BB[2], BD[2], BBp[2], BDp[2];
+  double FB[2], BB[2], BD[2], BBp[2], BDp[2], FD[2];
 #pragma unroll
   for (int ks = 0; ks < 2; ++ks) {
     const int i = 4 * ks + t;                 // forward: K = node index, column = point g
@@ -169,78 +160,27 @@ __global__ void __launch_bounds__(32 * WPE * EPC, 1)
     BBp[ks] = g < N ? __ldg(TB + ap * N + g) : 0.0;
     BDp[ks] = g < N ? __ldg(TD + ap * N + g) : 0.0;
   }
+  // folded fragments (E and O MMAs of XF / YF): row k = t = node pair (t < 3: (t, 6 - t); t = 3:
+  // the middle node), column n = g: n < 4 the B pair a = n, n >= 4 the D pair a = n - 4
+  const double* fB = tables + 2 * Q * N;
+  const double* fD = fB + FTS;
+  const double FEf = g < 4 ? __ldg(fB + g * 4 + t) : __ldg(fD + (g - 4) * 4 + t);
+  const double FOf = t < 3 ? (g < 4 ? __ldg(fB + 16 + g * 3 + t) : __ldg(fD + 16 + (g - 4) * 3 + t)) : 0.0;
 
-  const int ex = (int)(e % s.nx), ey = (int)((e / s.nx) % s.ny), ez = (int)(e / ((int64_t)s.nx * s.ny));
   const int64_t plane = (int64_t)s.Nx * s.Ny;
   const bool bc = s.faces != 0;
-  const int I0 = ex * P, J0 = ey * P, K0 = ez * P;
-  const int64_t ebase = I0 + (int64_t)s.Nx * J0 + plane * K0;
-  const int iK[2] = {t, (4 + t) < N ? 4 + t : N - 1};   // K index 4 ks + t, clamped (zero coefficient)
-
-  const double* qe = qd + e * (int64_t)QD_PER_ELEM;
-#if ELAS_TC_AQ_EARLY == 2
-  // the first slice's qdata is requested before the x stage so its latency hides behind it
-  double Aq[4][9];
-  {
-    const double* qs = qe + (NSLICE / WPE) * half * 4 * 9 * 32 + lane;
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int f = 0; f < 9; ++f) Aq[r][f] = __ldg(qs + (r * 9 + f) * 32);
-  }
-#endif
-
-  // ---------------- XF: gather + contraction in x (tiles T = half, half+2, ...) ----------
-  {
-    double a[XT_PER_WARP][2][2];  // all gathers of this warp issued before any MMA
-#pragma unroll
-    for (int u = 0; u < XT_PER_WARP; ++u)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        int c, j, k;
-        fibre(16 * (WPE * u + half) + g + 8 * h, c, j, k);
-        const double* src = x + c * s.nodes + ebase + (int64_t)s.Nx * j + plane * k;
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
-          const double v = __ldg(src + iK[ks]);
-          a[u][ks][h] = (bc && cons(I0 + iK[ks], J0 + j, K0 + k, s)) ? 0.0 : v;
-        }
-      }
-#pragma unroll
-    for (int u = 0; u < XT_PER_WARP; ++u) {
-      if (WPE * u + half >= XTILES) break;
-      double cb[4] = {0, 0, 0, 0}, cd[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        mma(cb, a[u][ks][0], a[u][ks][1], FB[ks]);
-        mma(cd, a[u][ks][0], a[u][ks][1], FD[ks]);
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int f = 16 * (WPE * u + half) + g + 8 * h;
-        int c, j, k;
-        fibre(f, c, j, k);
-        double* dst = UX + c * UX_C + uxo(k, j, 2 * t);
-        if (f < 3 * N * N) {
-          *reinterpret_cast<double2*>(dst) = make_double2(cb[2 * h], cb[2 * h + 1]);
-          *reinterpret_cast<double2*>(dst + UX_V) = make_double2(cd[2 * h], cd[2 * h + 1]);
-        }
-      }
-    }
-  }
-
   // lane constants of the slice stages (rows ff = g + 8h -> k = ff >> 1, a1l = ff & 1)
   const int gl = g & 1, gh = g >> 1;
   const int kr[2] = {gh, (gh + 4) < N ? gh + 4 : N - 1};
   const bool row1 = g + 8 < 2 * N;
-  const int sw_yf = (((t >> 1) & 1) << 2) | ((gh & 1) << 1);  // UX swizzle of (j = 4ks+t, k = kr[h])
   const int sw_yb = ((t & 1) << 2) | ((gh & 1) << 1);         // UX swizzle of (j = 2t+u, k = kr[h])
+  const int iK[2] = {t, (4 + t) < N ? 4 + t : N - 1};   // K index 4 ks + t, clamped (zero coefficient)
   int yfb[2][2], ybl[2][2], zfl[2][2], zbs[2][2], ybs[2][2], yfs[2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      yfb[a][h] = kr[h] * UX_K + iK[a] * UX_J + gl;          // YF load, a = ks
+      yfb[a][h] = kr[h] * UX_K + iK[a] * UX_J + gl;          // YF load (w0), a = ks
       ybl[a][h] = u2o(kr[h], gl, 4 * a + t);                   // YB load, a = ks
       zfl[a][h] = u2o(iK[a], h, g);                            // ZF load, a = ks
       zbs[a][h] = u2o((2 * t + a) < N ? 2 * t + a : N - 1, h, g);  // ZB store, a = u (k = 2t+u)
@@ -248,219 +188,309 @@ __global__ void __launch_bounds__(32 * WPE * EPC, 1)
     }
 #pragma unroll
   for (int h = 0; h < 2; ++h) yfs[h] = u2o(kr[h], gl, 2 * t);
-  pair_sync(el);
+  const int jlo = t, jhi = 6 - t;                              // folded node pair of this lane
 
-  const double re = __ldg(rr + e);
-
-#pragma unroll 1
-  for (int ss = 0; ss < NSLICE / WPE; ++ss) {
-    const int sl = (NSLICE / WPE) * half + ss;   // this warp's slices: a1 in {2 sl, 2 sl + 1}
-    const int xyf = (2 * sl) ^ sw_yf, xyb = (2 * sl) ^ sw_yb;
-    const double* qs = qe + sl * 4 * 9 * 32 + lane;   // qdata of this slice, fragment order
+  const int64_t stride = (int64_t)gridDim.x * EPC;
+  for (int64_t e = e_begin + (int64_t)blockIdx.x * EPC + el; e < e_end; e += stride) {
+    pair_sync(el);   // the previous element's XB is done with UX
+    const int ex = (int)(e % s.nx), ey = (int)((e / s.nx) % s.ny), ez = (int)(e / ((int64_t)s.nx * s.ny));
+    const int I0 = ex * P, J0 = ey * P, K0 = ez * P;
+    const int64_t ebase = I0 + (int64_t)s.Nx * J0 + plane * K0;
+    const double* qe = qd + e * (int64_t)QD_PER_ELEM;
 #if ELAS_L2_PREFETCH
-    if (ELAS_TC_PF == 3 && lane == 0 && ss + 1 < NSLICE / WPE)   // the warp's next slice -> L2
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qe + (sl + 1) * 4 * 9 * 32),
-                   "r"((uint32_t)(4 * 9 * 32 * 8)) : "memory");
-#endif
-    // rows h = 0 of the fused z stage: qdata of points r = 0, 1 requested before the y stage
-    double Aq[2][9];
+    {  // the slot's NEXT element: quadrature data (one bulk prefetch) and x rows into L2
+      const int64_t en = e + stride;
+      if (en < e_end) {
+        if (lane == 0 && half == 0)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qd + en * (int64_t)QD_PER_ELEM),
+                       "r"((uint32_t)(QD_PER_ELEM * 8)) : "memory");
+        const int nx_ = (int)(en % s.nx), ny_ = (int)((en / s.nx) % s.ny), nz_ = (int)(en / ((int64_t)s.nx * s.ny));
+        const int64_t nbase = nx_ * P + (int64_t)s.Nx * (ny_ * P) + plane * (nz_ * P);
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int f = 0; f < 9; ++f) Aq[r][f] = __ldg(qs + (r * 9 + f) * 32);
-
-    // ---------------- YF: contraction in y (fibres ff = 2k + a1l, 14 of 16 rows) ---------
-    {
-      double bx[3][2][2], dx[3][2][2];  // [c][ks][h]: UX0 = Bx u, UX1 = Dx u
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks)
+        for (int u = 0; u < XT_PER_WARP; ++u)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            bx[c][ks][h] = UX[c * UX_C + xyf + yfb[ks][h]];
-            dx[c][ks][h] = UX[c * UX_C + UX_V + xyf + yfb[ks][h]];
+            if (t == 0) {   // one lane per fibre row (a row is 56 B)
+              int c, j, k;
+              fibre(16 * (WPE * u + half) + g + 8 * h, c, j, k);
+              const double* src = x + c * s.nodes + nbase + (int64_t)s.Nx * j + plane * k;
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(src + N - 1));
+            }
           }
-      double w[3][3][4];
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int v = 0; v < 3; ++v)
-#pragma unroll
-          for (int r = 0; r < 4; ++r) w[c][v][r] = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          mma(w[c][0], dx[c][ks][0], dx[c][ks][1], FB[ks]);  // (Dx, By)
-          mma(w[c][1], bx[c][ks][0], bx[c][ks][1], FD[ks]);  // (Bx, Dy)
-          mma(w[c][2], bx[c][ks][0], bx[c][ks][1], FB[ks]);  // (Bx, By)
-        }
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int v = 0; v < 3; ++v) {
-          double* ob = U2 + c * U2_C + v * U2_W;
-          *reinterpret_cast<double2*>(ob + yfs[0]) = make_double2(w[c][v][0], w[c][v][1]);
-          if (row1) *reinterpret_cast<double2*>(ob + yfs[1]) = make_double2(w[c][v][2], w[c][v][3]);
-        }
+      }
     }
-    __syncwarp();
+#endif
 
-    // ---------------- fused z stage, one 8-row half (a1l = h) at a time ---------------
-    // ZF: rows phi = g -> (a1l = h, a2 = g); cols a3 = 2t, 2t+1  -> gradients G[c][d][2]
-    // pointwise on the two points (a1l = h, a2 = g, a3 = 2t + u), qdata r = 2h + u
-    // ZB: K position (ks, t) <-> a3 = 2t + ks, A operand straight from G; rows -> U2 rows
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      double G[3][3][2];
-      {
-        double zi[3][3][2];  // [c][w][ks]
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int w = 0; w < 3; ++w)
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) zi[c][w][ks] = U2[c * U2_C + w * U2_W + zfl[ks][h]];
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int w = 0; w < 3; ++w) G[c][w][0] = G[c][w][1] = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int w = 0; w < 3; ++w) mma8(G[c][w], zi[c][w][ks], w == 2 ? FD[ks] : FB[ks]);
-      }
-      double An[2][9];   // qdata of the other half, requested now (consumed next iteration)
-      if (h == 0) {
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-          for (int f = 0; f < 9; ++f) An[r][f] = __ldg(qs + ((2 + r) * 9 + f) * 32);
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        double Gp[3][3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int d = 0; d < 3; ++d) Gp[c][d] = G[c][d][u];
-        pointwise(Gp, Aq[u], re);
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int d = 0; d < 3; ++d) G[c][d][u] = Gp[c][d];
-      }
-      if (h == 0) {
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-          for (int f = 0; f < 9; ++f) Aq[r][f] = An[r][f];
-      }
-      __syncwarp();  // every lane has read its ZF inputs of rows h before they are overwritten
-      double v[3][3][2];
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) v[c][d][0] = v[c][d][1] = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int d = 0; d < 3; ++d) mma8(v[c][d], G[c][d][ks], d == 2 ? BDp[ks] : BBp[ks]);
-      // rows (a1l = h, a2 = g), cols k = 2t, 2t+1
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          double* ob = U2 + c * U2_C + d * U2_W;
-          ob[zbs[0][h]] = v[c][d][0];
-          if (t < 3) ob[zbs[1][h]] = v[c][d][1];
-        }
-    }
-    __syncwarp();
-
-    // ---------------- YB: transposed y -> T0, T1 into UX (this slice's a1 columns) ------
+    // ---------------- XF: gather + folded contraction in x (tiles T = half, half+2, ...) -----
     {
-      double vi[3][3][2][2];  // [c][d][ks][h]
+      double up[XT_PER_WARP][2], um[XT_PER_WARP][2];  // [tile][h]: all gathers issued before any MMA
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int d = 0; d < 3; ++d)
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) vi[c][d][ks][h] = U2[c * U2_C + d * U2_W + ybl[ks][h]];
-      double t0[3][4], t1[3][4];
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) t0[c][r] = t1[c][r] = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          mma(t0[c], vi[c][0][ks][0], vi[c][0][ks][1], BB[ks]);   // By^T V0
-          mma(t1[c], vi[c][1][ks][0], vi[c][1][ks][1], BD[ks]);   // Dy^T V1
-        }
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) mma(t1[c], vi[c][2][ks][0], vi[c][2][ks][1], BB[ks]);  // + By^T V2
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double* ob = UX + c * UX_C + xyb;
+      for (int u = 0; u < XT_PER_WARP; ++u)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          if (h == 0 || row1) {
-            ob[ybs[0][h]] = t0[c][2 * h];
-            ob[UX_V + ybs[0][h]] = t1[c][2 * h];
-            if (t < 3) {
-              ob[ybs[1][h]] = t0[c][2 * h + 1];
-              ob[UX_V + ybs[1][h]] = t1[c][2 * h + 1];
+          int c, j, k;
+          fibre(16 * (WPE * u + half) + g + 8 * h, c, j, k);
+          const double* src = x + c * s.nodes + ebase + (int64_t)s.Nx * j + plane * k;
+          double lo = __ldg(src + jlo), hi = __ldg(src + jhi);
+          if (bc) {
+            if (cons(I0 + jlo, J0 + j, K0 + k, s)) lo = 0.0;
+            if (cons(I0 + jhi, J0 + j, K0 + k, s)) hi = 0.0;
+          }
+          up[u][h] = t < 3 ? lo + hi : lo;
+          um[u][h] = t < 3 ? lo - hi : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < XT_PER_WARP; ++u) {
+        if (WPE * u + half >= XTILES) break;
+        double cE[4] = {0, 0, 0, 0}, cO[4] = {0, 0, 0, 0};
+        mma(cE, up[u][0], up[u][1], FEf);
+        mma(cO, um[u][0], um[u][1], FOf);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int f = 16 * (WPE * u + half) + g + 8 * h;
+          if (f < 3 * N * N) {
+            int c, j, k;
+            fibre(f, c, j, k);
+            const int tab = t >> 1;                    // column pair 2t, 2t+1 -> table, pairs a
+            double* dst = UX + c * UX_C + tab * UX_V;
+#pragma unroll
+            for (int uu = 0; uu < 2; ++uu) {
+              const int a = 2 * (t & 1) + uu;
+              const double E = cE[2 * h + uu], O = cO[2 * h + uu];
+              dst[uxo(k, j, a)] = E + O;
+              dst[uxo(k, j, 7 - a)] = tab == 0 ? E - O : O - E;
             }
           }
         }
       }
     }
-    __syncwarp();
-  }
-  pair_sync(el);
+    pair_sync(el);
 
-  // ---------------- XB: transposed x + scatter-add (tiles T = half, half+2, ...) ---------
+    const double re = __ldg(rr + e);
+
+#pragma unroll 1
+    for (int ss = 0; ss < NSLICE / WPE; ++ss) {
+      const int sl = (NSLICE / WPE) * half + ss;   // this warp's slices: a1 in {2 sl, 2 sl + 1}
+      const int sw_yf = (((t >> 1) & 1) << 2) | ((gh & 1) << 1);
+      const int xyf = (2 * sl) ^ sw_yf, xyb = (2 * sl) ^ sw_yb;
+      const double* qs = qe + sl * 4 * 9 * 32 + lane;   // qdata of this slice, fragment order
+      // rows h = 0 of the fused z stage: qdata of points r = 0, 1 requested before the y stage
+      double Aq[2][9];
 #pragma unroll
-  for (int u = 0; u < XT_PER_WARP; ++u) {
-    if (WPE * u + half >= XTILES) break;
-    int cc[2], jj[2], kk[2];
-    bool okr[2];
+      for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int f = 16 * (WPE * u + half) + g + 8 * h;
-      okr[h] = f < 3 * N * N;
-      fibre(f, cc[h], jj[h], kk[h]);
+        for (int f = 0; f < 9; ++f) Aq[r][f] = __ldg(qs + (r * 9 + f) * 32);
+
+      // ---------------- YF: contraction in y (fibres ff = 2k + a1l, 14 of 16 rows) ---------
+      {
+        double dx[3][2][2];             // [c][ks][h]: UX1 = Dx u (plain, K = j)
+        double bp[3][2], bm[3][2];      // [c][h]: UX0 = Bx u folded over j (K = node pair)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) dx[c][ks][h] = UX[c * UX_C + UX_V + xyf + yfb[ks][h]];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int a1 = 2 * sl + gl;
+            const double lo = UX[c * UX_C + uxo(kr[h], jlo, a1)];
+            const double hi = UX[c * UX_C + uxo(kr[h], jhi, a1)];
+            bp[c][h] = t < 3 ? lo + hi : lo;
+            bm[c][h] = t < 3 ? lo - hi : 0.0;
+          }
+        }
+        double w0[3][4], wE[3][4], wO[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) w0[c][r] = wE[c][r] = wO[c][r] = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          mma(w0[c], dx[c][0][0], dx[c][0][1], FB[0]);   // (Dx, By)
+          mma(wE[c], bp[c][0], bp[c][1], FEf);           // (Bx, By) | (Bx, Dy), even part
+          mma(w0[c], dx[c][1][0], dx[c][1][1], FB[1]);
+          mma(wO[c], bm[c][0], bm[c][1], FOf);           // odd part
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double* o0 = U2 + c * U2_C;
+          *reinterpret_cast<double2*>(o0 + yfs[0]) = make_double2(w0[c][0], w0[c][1]);
+          if (row1) *reinterpret_cast<double2*>(o0 + yfs[1]) = make_double2(w0[c][2], w0[c][3]);
+          // columns 2t, 2t+1: t < 2 -> By pairs (w2 = (Bx, By)), t >= 2 -> Dy pairs (w1 = (Bx, Dy))
+          const int tab = t >> 1;
+          double* ob = U2 + c * U2_C + (tab == 0 ? 2 : 1) * U2_W;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !row1) continue;
+#pragma unroll
+            for (int uu = 0; uu < 2; ++uu) {
+              const int a = 2 * (t & 1) + uu;
+              const double E = wE[c][2 * h + uu], O = wO[c][2 * h + uu];
+              ob[u2o(kr[h], gl, a)] = E + O;
+              ob[u2o(kr[h], gl, 7 - a)] = tab == 0 ? E - O : O - E;
+            }
+          }
+        }
+      }
+      __syncwarp();
+
+      // ---------------- fused z stage, one 8-row half (a1l = h) at a time ---------------
+      // ZF: rows phi = g -> (a1l = h, a2 = g); cols a3 = 2t, 2t+1  -> gradients G[c][d][2]
+      // pointwise on the two points (a1l = h, a2 = g, a3 = 2t + u), qdata r = 2h + u
+      // ZB: K position (ks, t) <-> a3 = 2t + ks, A operand straight from G; rows -> U2 rows
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double G[3][3][2];
+        {
+          double zi[3][3][2];  // [c][w][ks]
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int w = 0; w < 3; ++w)
+#pragma unroll
+              for (int ks = 0; ks < 2; ++ks) zi[c][w][ks] = U2[c * U2_C + w * U2_W + zfl[ks][h]];
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int w = 0; w < 3; ++w) G[c][w][0] = G[c][w][1] = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+              for (int w = 0; w < 3; ++w) mma8(G[c][w], zi[c][w][ks], w == 2 ? FD[ks] : FB[ks]);
+        }
+        double An[2][9];   // qdata of the other half, requested now (consumed next iteration)
+        if (h == 0) {
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int f = 0; f < 9; ++f) An[r][f] = __ldg(qs + ((2 + r) * 9 + f) * 32);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          double Gp[3][3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) Gp[c][d] = G[c][d][u];
+          pointwise(Gp, Aq[u], re);
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) G[c][d][u] = Gp[c][d];
+        }
+        if (h == 0) {
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int f = 0; f < 9; ++f) Aq[r][f] = An[r][f];
+        }
+        __syncwarp();  // every lane has read its ZF inputs of rows h before they are overwritten
+        double v[3][3][2];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) v[c][d][0] = v[c][d][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) mma8(v[c][d], G[c][d][ks], d == 2 ? BDp[ks] : BBp[ks]);
+        // rows (a1l = h, a2 = g), cols k = 2t, 2t+1
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            double* ob = U2 + c * U2_C + d * U2_W;
+            ob[zbs[0][h]] = v[c][d][0];
+            if (t < 3) ob[zbs[1][h]] = v[c][d][1];
+          }
+      }
+      __syncwarp();
+
+      // ---------------- YB: transposed y -> T0, T1 into UX (this slice's a1 columns) ------
+      {
+        double vi[3][3][2][2];  // [c][d][ks][h]
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) vi[c][d][ks][h] = U2[c * U2_C + d * U2_W + ybl[ks][h]];
+        double t0[3][4], t1[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) t0[c][r] = t1[c][r] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            mma(t0[c], vi[c][0][ks][0], vi[c][0][ks][1], BB[ks]);   // By^T V0
+            mma(t1[c], vi[c][1][ks][0], vi[c][1][ks][1], BD[ks]);   // Dy^T V1
+          }
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) mma(t1[c], vi[c][2][ks][0], vi[c][2][ks][1], BB[ks]);  // + By^T V2
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double* ob = UX + c * UX_C + xyb;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h == 0 || row1) {
+              ob[ybs[0][h]] = t0[c][2 * h];
+              ob[UX_V + ybs[0][h]] = t1[c][2 * h];
+              if (t < 3) {
+                ob[ybs[1][h]] = t0[c][2 * h + 1];
+                ob[UX_V + ybs[1][h]] = t1[c][2 * h + 1];
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
     }
-    double o[4] = {0, 0, 0, 0};
+    pair_sync(el);
+
+    // ---------------- XB: transposed x + scatter-add (tiles T = half, half+2, ...) ---------
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      const int a1 = 4 * ks + t;
-      const double* r0 = UX + cc[0] * UX_C + uxo(kk[0], jj[0], a1);
-      const double* r1 = UX + cc[1] * UX_C + uxo(kk[1], jj[1], a1);
-      mma(o, r0[0], r1[0], BD[ks]);         // Dx^T T0
-      mma(o, r0[UX_V], r1[UX_V], BB[ks]);   // Bx^T T1
-    }
+    for (int u = 0; u < XT_PER_WARP; ++u) {
+      if (WPE * u + half >= XTILES) break;
+      int cc[2], jj[2], kk[2];
+      bool okr[2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (!okr[h]) continue;
-      double* dst = y + cc[h] * s.nodes + ebase + (int64_t)s.Nx * jj[h] + plane * kk[h];
+      for (int h = 0; h < 2; ++h) {
+        const int f = 16 * (WPE * u + half) + g + 8 * h;
+        okr[h] = f < 3 * N * N;
+        fibre(f, cc[h], jj[h], kk[h]);
+      }
+      double o[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int uu = 0; uu < 2; ++uu) {
-        const int i = 2 * t + uu;
-        if (i >= N) continue;
-        if (bc && cons(I0 + i, J0 + jj[h], K0 + kk[h], s)) continue;
-        atomicAdd(dst + i, o[2 * h + uu]);
+      for (int ks = 0; ks < 2; ++ks) {
+        const int a1 = 4 * ks + t;
+        const double* r0 = UX + cc[0] * UX_C + uxo(kk[0], jj[0], a1);
+        const double* r1 = UX + cc[1] * UX_C + uxo(kk[1], jj[1], a1);
+        mma(o, r0[0], r1[0], BD[ks]);         // Dx^T T0
+        mma(o, r0[UX_V], r1[UX_V], BB[ks]);   // Bx^T T1
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!okr[h]) continue;
+        double* dst = y + cc[h] * s.nodes + ebase + (int64_t)s.Nx * jj[h] + plane * kk[h];
+#pragma unroll
+        for (int uu = 0; uu < 2; ++uu) {
+          const int i = 2 * t + uu;
+          if (i >= N) continue;
+          if (bc && cons(I0 + i, J0 + jj[h], K0 + kk[h], s)) continue;
+          atomicAdd(dst + i, o[2 * h + uu]);
+        }
       }
     }
   }
