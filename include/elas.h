@@ -253,6 +253,20 @@ int elas_pcg(elas_op* op, int precond, elas_cheb* cheb, const double* b, double*
  * host.  This is the reduction elas_pcg and the power iteration use. */
 int elas_dot(elas_op* op, const double* a, const double* b, double* result);
 
+/* NVLink peer-store interface sum (SURVEY 8(e) extra; PAPER.md:604 names the parallel exchange as
+ * the next bottleneck).  COLLECTIVE over the op's NCCL communicator: every rank calls it with the
+ * same `on`.  on = 1: the ranks exchange CUDA IPC handles of their halo buffers and of a small
+ * flag buffer with their z-neighbours (once; the mapping is kept until elas_destroy), and from
+ * then on every interface sum of this op (elas_apply, elas_diagonal, the GMG restriction) copies
+ * the rank's partial interface plane straight into the neighbour's halo over NVLink and
+ * publishes it with a release store of the exchange epoch into the neighbour's flag; the
+ * receiver's stream waits on its own flag (a one-thread spin kernel, so both GPUs must run
+ * concurrently: one process per GPU) before the same plane-add as the NCCL path, then tells the
+ * sender its halo may be overwritten.  Results are bitwise equal to the NCCL path.  on = 0:
+ * back to NCCL send/recv.  ELAS_EINVAL for ops without a communicator (nranks == 1, external
+ * mode); CUDA errors if the neighbours' memory cannot be mapped (e.g. ranks in one process). */
+int elas_set_peer_exchange(elas_op* op, int on);
+
 /* Geometric multigrid V-cycle (Sec. 3, Fig. 2).
  * Readings R22-R25 in DESIGN.md.  Z-slabs (fine->nranks > 1): nz must be divisible by
  * nranks * 2^(levels-1) so every level's slabs align (coarse slab = fine slab / 2); every level

@@ -151,6 +151,9 @@ void free_op(elas_op* op) {
   cudaFree(op->cc);
   cudaFree(op->xs);
   cudaFree(op->ys);
+  for (void* pp : {(void*)op->peer_lo_halo, (void*)op->peer_lo_flags, (void*)op->peer_hi_halo, (void*)op->peer_hi_flags})
+    if (pp) cudaIpcCloseMemHandle(pp);
+  cudaFree(op->peer_flags);
   cudaFree(op->halo_lo);
   cudaFree(op->halo_hi);
   if (op->comm && !op->comm_borrowed) ncclCommDestroy(op->comm);
@@ -367,7 +370,16 @@ int attach_comm(elas_op* op, ncclComm_t comm) {
   return ELAS_OK;
 }
 
-int exchange_planes(elas_op* op, double* y) {
+// The interface sum (A6, PAPER.md:169 P^T) in two halves around the interior elements.
+// begin: after the boundary layers, the partial interface planes of y leave on the comm stream --
+//   NCCL send/recv into the neighbours' halo buffers, or (peer mode, elas_set_peer_exchange) a
+//   direct copy into the neighbour's IPC-mapped halo over NVLink followed by a release store of
+//   the exchange epoch into the neighbour's flag;
+// end: the received halos are added into y (the same plane-add kernel in both modes, so the
+//   replicated planes are bitwise equal: a + b on one rank, b + a on the other).  Peer mode first
+//   waits on the flag the neighbour set (a one-thread kernel spinning on its own device memory,
+//   written by the other GPU), then tells the neighbour its halo may be overwritten again.
+int exchange_begin(elas_op* op, double* y) {
   if (op->nranks == 1 || op->external) return ELAS_OK;
   const Slab& s = op->slab;
   cudaStream_t st = op->stream;
@@ -375,24 +387,66 @@ int exchange_planes(elas_op* op, double* y) {
   const int64_t plane = (int64_t)s.Nx * s.Ny;
   CUDA_OR(cudaEventRecord(op->ev_boundary, st), "cudaEventRecord");
   CUDA_OR(cudaStreamWaitEvent(op->comm_stream, op->ev_boundary, 0), "cudaStreamWaitEvent");
-  NCCL_OR(ncclGroupStart(), "ncclGroupStart");
-  for (int c = 0; c < 3; ++c) {
-    if (lo) {
-      NCCL_OR(ncclSend(y + c * s.nodes, plane, ncclDouble, op->rank - 1, op->comm, op->comm_stream), "ncclSend");
-      NCCL_OR(ncclRecv(op->halo_lo + c * plane, plane, ncclDouble, op->rank - 1, op->comm, op->comm_stream), "ncclRecv");
+  if (op->peer_on) {
+    const unsigned long long ep = ++op->peer_epoch;
+    cudaStream_t cs = op->comm_stream;
+    if (lo) {   // my bottom plane -> the lower rank's halo_hi
+      CUDA_OR(launch_wait_flag(op->peer_flags + PF_CONSUMED_LO, ep - 1, cs), "peer wait");
+      for (int c = 0; c < 3; ++c)
+        CUDA_OR(cudaMemcpyAsync(op->peer_lo_halo + c * plane, y + c * s.nodes, sizeof(double) * plane,
+                                cudaMemcpyDeviceToDevice, cs), "peer copy");
+      CUDA_OR(launch_signal_flag(op->peer_lo_flags + PF_FILLED_HI, ep, cs), "peer signal");
     }
-    if (hi) {
-      NCCL_OR(ncclSend(y + c * s.nodes + (int64_t)(s.Nz - 1) * plane, plane, ncclDouble, op->rank + 1, op->comm,
-                       op->comm_stream), "ncclSend");
-      NCCL_OR(ncclRecv(op->halo_hi + c * plane, plane, ncclDouble, op->rank + 1, op->comm, op->comm_stream), "ncclRecv");
+    if (hi) {   // my top plane -> the upper rank's halo_lo
+      CUDA_OR(launch_wait_flag(op->peer_flags + PF_CONSUMED_HI, ep - 1, cs), "peer wait");
+      for (int c = 0; c < 3; ++c)
+        CUDA_OR(cudaMemcpyAsync(op->peer_hi_halo + c * plane, y + c * s.nodes + (int64_t)(s.Nz - 1) * plane,
+                                sizeof(double) * plane, cudaMemcpyDeviceToDevice, cs), "peer copy");
+      CUDA_OR(launch_signal_flag(op->peer_hi_flags + PF_FILLED_LO, ep, cs), "peer signal");
     }
+  } else {
+    NCCL_OR(ncclGroupStart(), "ncclGroupStart");
+    for (int c = 0; c < 3; ++c) {
+      if (lo) {
+        NCCL_OR(ncclSend(y + c * s.nodes, plane, ncclDouble, op->rank - 1, op->comm, op->comm_stream), "ncclSend");
+        NCCL_OR(ncclRecv(op->halo_lo + c * plane, plane, ncclDouble, op->rank - 1, op->comm, op->comm_stream), "ncclRecv");
+      }
+      if (hi) {
+        NCCL_OR(ncclSend(y + c * s.nodes + (int64_t)(s.Nz - 1) * plane, plane, ncclDouble, op->rank + 1, op->comm,
+                         op->comm_stream), "ncclSend");
+        NCCL_OR(ncclRecv(op->halo_hi + c * plane, plane, ncclDouble, op->rank + 1, op->comm, op->comm_stream), "ncclRecv");
+      }
+    }
+    NCCL_OR(ncclGroupEnd(), "ncclGroupEnd");
   }
-  NCCL_OR(ncclGroupEnd(), "ncclGroupEnd");
   CUDA_OR(cudaEventRecord(op->ev_comm, op->comm_stream), "cudaEventRecord");
-  CUDA_OR(cudaStreamWaitEvent(st, op->ev_comm, 0), "cudaStreamWaitEvent");
-  if (lo) CUDA_OR(launch_plane_add(s, 0, y, op->halo_lo, st), "plane add launch");
-  if (hi) CUDA_OR(launch_plane_add(s, s.Nz - 1, y, op->halo_hi, st), "plane add launch");
   return ELAS_OK;
+}
+
+int exchange_end(elas_op* op, double* y) {
+  if (op->nranks == 1 || op->external) return ELAS_OK;
+  const Slab& s = op->slab;
+  cudaStream_t st = op->stream;
+  const bool lo = op->rank > 0, hi = op->rank < op->nranks - 1;
+  // my own sends are done with y's boundary planes before anything later on st writes them
+  CUDA_OR(cudaStreamWaitEvent(st, op->ev_comm, 0), "cudaStreamWaitEvent");
+  const unsigned long long ep = op->peer_epoch;
+  if (lo) {
+    if (op->peer_on) CUDA_OR(launch_wait_flag(op->peer_flags + PF_FILLED_LO, ep, st), "peer wait");
+    CUDA_OR(launch_plane_add(s, 0, y, op->halo_lo, st), "plane add launch");
+    if (op->peer_on) CUDA_OR(launch_signal_flag(op->peer_lo_flags + PF_CONSUMED_HI, ep, st), "peer signal");
+  }
+  if (hi) {
+    if (op->peer_on) CUDA_OR(launch_wait_flag(op->peer_flags + PF_FILLED_HI, ep, st), "peer wait");
+    CUDA_OR(launch_plane_add(s, s.Nz - 1, y, op->halo_hi, st), "plane add launch");
+    if (op->peer_on) CUDA_OR(launch_signal_flag(op->peer_hi_flags + PF_CONSUMED_LO, ep, st), "peer signal");
+  }
+  return ELAS_OK;
+}
+
+int exchange_planes(elas_op* op, double* y) {
+  int rc = exchange_begin(op, y);
+  return rc ? rc : exchange_end(op, y);
 }
 
 }  // namespace elas
@@ -400,6 +454,64 @@ int exchange_planes(elas_op* op, double* y) {
 extern "C" {
 
 int elas_version(void) { return ELAS_VERSION; }
+
+int elas_set_peer_exchange(elas_op* op, int on) {
+  if (!op) { set_error("elas_set_peer_exchange: NULL op"); return ELAS_EINVAL; }
+  if (op->nranks < 2 || op->external || !op->comm) {
+    set_error("elas_set_peer_exchange: needs an NCCL-mode slab operator (nranks > 1, nccl_id given)");
+    return ELAS_EINVAL;
+  }
+  if (!on) { op->peer_on = false; return ELAS_OK; }
+  if (op->peer_flags) { op->peer_on = true; return ELAS_OK; }
+  const bool lo = op->rank > 0, hi = op->rank < op->nranks - 1;
+  CUDA_OR(cudaStreamSynchronize(op->stream), "cudaStreamSynchronize");
+  CUDA_OR(cudaStreamSynchronize(op->comm_stream), "cudaStreamSynchronize");
+  CUDA_OR(cudaMalloc(&op->peer_flags, sizeof(unsigned long long) * elas::PF_COUNT), "cudaMalloc (peer flags)");
+  CUDA_OR(cudaMemset(op->peer_flags, 0, sizeof(unsigned long long) * elas::PF_COUNT), "cudaMemset (peer flags)");
+  // my IPC handles: halo_lo, halo_hi, flags -> both neighbours (NCCL send/recv of the bytes; the
+  // exchange also orders every rank's zeroed flags before any neighbour can signal them)
+  cudaIpcMemHandle_t mine[3], from_lo[3], from_hi[3];
+  CUDA_OR(cudaIpcGetMemHandle(&mine[0], op->halo_lo), "cudaIpcGetMemHandle");
+  CUDA_OR(cudaIpcGetMemHandle(&mine[1], op->halo_hi), "cudaIpcGetMemHandle");
+  CUDA_OR(cudaIpcGetMemHandle(&mine[2], op->peer_flags), "cudaIpcGetMemHandle");
+  const size_t hb = sizeof(mine);
+  char* dbuf = nullptr;
+  CUDA_OR(cudaMalloc(&dbuf, 3 * hb), "cudaMalloc (handle exchange)");
+  CUDA_OR(cudaMemcpy(dbuf, mine, hb, cudaMemcpyHostToDevice), "cudaMemcpy");
+  ncclResult_t nr = ncclGroupStart();
+  if (nr == ncclSuccess && lo) {
+    nr = ncclSend(dbuf, hb, ncclInt8, op->rank - 1, op->comm, op->comm_stream);
+    if (nr == ncclSuccess) nr = ncclRecv(dbuf + hb, hb, ncclInt8, op->rank - 1, op->comm, op->comm_stream);
+  }
+  if (nr == ncclSuccess && hi) {
+    nr = ncclSend(dbuf, hb, ncclInt8, op->rank + 1, op->comm, op->comm_stream);
+    if (nr == ncclSuccess) nr = ncclRecv(dbuf + 2 * hb, hb, ncclInt8, op->rank + 1, op->comm, op->comm_stream);
+  }
+  ncclResult_t ne = ncclGroupEnd();
+  cudaError_t ce = cudaStreamSynchronize(op->comm_stream);
+  if (ce == cudaSuccess) ce = cudaMemcpy(from_lo, dbuf + hb, hb, cudaMemcpyDeviceToHost);
+  if (ce == cudaSuccess) ce = cudaMemcpy(from_hi, dbuf + 2 * hb, hb, cudaMemcpyDeviceToHost);
+  cudaFree(dbuf);
+  if (nr != ncclSuccess) return nccl_fail(nr, "handle exchange");
+  if (ne != ncclSuccess) return nccl_fail(ne, "handle exchange");
+  if (ce != cudaSuccess) return cuda_fail(ce, "handle exchange");
+  void* ptr = nullptr;
+  if (lo) {   // the lower rank's halo_hi (my bottom plane goes there) and its flags
+    CUDA_OR(cudaIpcOpenMemHandle(&ptr, from_lo[1], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    op->peer_lo_halo = static_cast<double*>(ptr);
+    CUDA_OR(cudaIpcOpenMemHandle(&ptr, from_lo[2], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    op->peer_lo_flags = static_cast<unsigned long long*>(ptr);
+  }
+  if (hi) {   // the upper rank's halo_lo and its flags
+    CUDA_OR(cudaIpcOpenMemHandle(&ptr, from_hi[0], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    op->peer_hi_halo = static_cast<double*>(ptr);
+    CUDA_OR(cudaIpcOpenMemHandle(&ptr, from_hi[2], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    op->peer_hi_flags = static_cast<unsigned long long*>(ptr);
+  }
+  op->peer_epoch = 0;
+  op->peer_on = true;
+  return ELAS_OK;
+}
 
 int elas_nccl_unique_id(void* id_out) {
   if (!id_out) { set_error("elas_nccl_unique_id: NULL output"); return ELAS_EINVAL; }
@@ -639,28 +751,9 @@ int elas_apply(elas_op* op, const double* x, double* y) {
   if (lo) { if ((rc = range_apply(op, x, y, 0, layer, st))) return rc; int0 = layer; }
   if (hi && ne - layer >= int0) { if ((rc = range_apply(op, x, y, ne - layer, ne, st))) return rc; int1 = ne - layer; }
   else if (hi) int1 = int0;
-  CUDA_OR(cudaEventRecord(op->ev_boundary, st), "cudaEventRecord");
-  CUDA_OR(cudaStreamWaitEvent(op->comm_stream, op->ev_boundary, 0), "cudaStreamWaitEvent");
-  const int64_t plane = (int64_t)s.Nx * s.Ny;
-  NCCL_OR(ncclGroupStart(), "ncclGroupStart");
-  for (int c = 0; c < 3; ++c) {
-    if (lo) {
-      NCCL_OR(ncclSend(y + c * s.nodes, plane, ncclDouble, op->rank - 1, op->comm, op->comm_stream), "ncclSend");
-      NCCL_OR(ncclRecv(op->halo_lo + c * plane, plane, ncclDouble, op->rank - 1, op->comm, op->comm_stream), "ncclRecv");
-    }
-    if (hi) {
-      NCCL_OR(ncclSend(y + c * s.nodes + (int64_t)(s.Nz - 1) * plane, plane, ncclDouble, op->rank + 1, op->comm,
-                       op->comm_stream), "ncclSend");
-      NCCL_OR(ncclRecv(op->halo_hi + c * plane, plane, ncclDouble, op->rank + 1, op->comm, op->comm_stream), "ncclRecv");
-    }
-  }
-  NCCL_OR(ncclGroupEnd(), "ncclGroupEnd");
-  CUDA_OR(cudaEventRecord(op->ev_comm, op->comm_stream), "cudaEventRecord");
+  if ((rc = elas::exchange_begin(op, y))) return rc;     // overlapped with the interior elements
   if ((rc = range_apply(op, x, y, int0, int1, st))) return rc;
-  CUDA_OR(cudaStreamWaitEvent(st, op->ev_comm, 0), "cudaStreamWaitEvent");
-  if (lo) CUDA_OR(elas::launch_plane_add(s, 0, y, op->halo_lo, st), "plane add launch");
-  if (hi) CUDA_OR(elas::launch_plane_add(s, s.Nz - 1, y, op->halo_hi, st), "plane add launch");
-  return ELAS_OK;
+  return elas::exchange_end(op, y);
 }
 
 int elas_apply_add(elas_op* op, const double* x, double* y) {

@@ -107,6 +107,10 @@ cudaError_t launch_face_copy(const Slab& s, const double* x, double* y, cudaStre
 cudaError_t launch_face_add(const Slab& s, const double* x, double* y, cudaStream_t st);
 cudaError_t launch_plane_add(const Slab& s, int which_plane, double* y, const double* halo,
                              cudaStream_t st);
+// peer-mode interface exchange: one thread spins (acquire, system scope) until *flag >= target;
+// one thread stores value into a (possibly peer, IPC-mapped) flag with release semantics
+cudaError_t launch_wait_flag(const unsigned long long* flag, unsigned long long target, cudaStream_t st);
+cudaError_t launch_signal_flag(unsigned long long* flag, unsigned long long value, cudaStream_t st);
 
 // error helpers
 void set_error(const std::string& msg);

@@ -34,6 +34,15 @@ struct elas_op {
   cudaEvent_t ev_boundary = nullptr, ev_comm = nullptr;
   double* halo_lo = nullptr;
   double* halo_hi = nullptr;
+  // NVLink peer-store interface sum (elas_set_peer_exchange): my flags (PF_*), the neighbours'
+  // IPC-mapped halo buffers and flags, the exchange epoch
+  bool peer_on = false;
+  unsigned long long peer_epoch = 0;
+  unsigned long long* peer_flags = nullptr;
+  double* peer_lo_halo = nullptr;           // the lower rank's halo_hi
+  double* peer_hi_halo = nullptr;           // the upper rank's halo_lo
+  unsigned long long* peer_lo_flags = nullptr;
+  unsigned long long* peer_hi_flags = nullptr;
   // measurement hook
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;   // pairs (start, stop), reused
@@ -70,6 +79,11 @@ int pcg_core(elas_op* op, int kind, const PrecondFn& M, const double* b, double*
 // exchange the partial interface planes of y with the neighbour ranks and add them (NCCL mode,
 // synchronous on the op's stream); no-op for nranks == 1 or external mode
 int exchange_planes(elas_op* op, double* y);
+// the two halves of exchange_planes around the interior elements (elas_apply)
+int exchange_begin(elas_op* op, double* y);
+int exchange_end(elas_op* op, double* y);
+// peer-mode flags (elas_op::peer_flags): written by the neighbours over NVLink
+enum { PF_FILLED_LO = 0, PF_FILLED_HI = 1, PF_CONSUMED_LO = 2, PF_CONSUMED_HI = 3, PF_COUNT = 4 };
 // make an external-mode slab op (nranks > 1, no communicator) an NCCL-mode op on a borrowed
 // communicator (GMG levels share the finest level's); the op does not destroy it
 int attach_comm(elas_op* op, ncclComm_t comm);

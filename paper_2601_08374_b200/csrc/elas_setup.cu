@@ -145,6 +145,19 @@ __global__ void plane_add_kernel(Slab s, int K, double* __restrict__ y, const do
   }
 }
 
+__global__ void wait_flag_kernel(const unsigned long long* flag, unsigned long long target) {
+  unsigned long long v;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= target) break;
+    __nanosleep(128);
+  }
+}
+
+__global__ void signal_flag_kernel(unsigned long long* flag, unsigned long long value) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+}
+
 int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   const int64_t cap = 148 * 32;
@@ -250,6 +263,17 @@ cudaError_t launch_face_add(const Slab& s, const double* x, double* y, cudaStrea
 cudaError_t launch_plane_add(const Slab& s, int which_plane, double* y, const double* halo, cudaStream_t st) {
   const int64_t n = 3 * (int64_t)s.Nx * s.Ny;
   plane_add_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, which_plane, y, halo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait_flag(const unsigned long long* flag, unsigned long long target, cudaStream_t st) {
+  if (target == 0) return cudaSuccess;   // nothing to wait for (first exchange)
+  wait_flag_kernel<<<1, 1, 0, st>>>(flag, target);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_signal_flag(unsigned long long* flag, unsigned long long value, cudaStream_t st) {
+  signal_flag_kernel<<<1, 1, 0, st>>>(flag, value);
   return cudaGetLastError();
 }
 

@@ -32,7 +32,8 @@ EXPORTED = ["elas_create", "elas_apply", "elas_apply_host", "elas_interface_add"
             "elas_diagonal", "elas_cheb_create", "elas_cheb_lambda_max", "elas_cheb_apply",
             "elas_cheb_destroy", "elas_pcg", "elas_gmg_create", "elas_gmg_level_op", "elas_gmg_levels",
             "elas_gmg_set_stream", "elas_gmg_apply", "elas_pcg_gmg", "elas_gmg_destroy", "elas_gmg_transfer",
-            "elas_set_deterministic", "elas_dot", "elas_create_aniso", "elas_apply_add"]
+            "elas_set_deterministic", "elas_dot", "elas_create_aniso", "elas_apply_add",
+            "elas_set_peer_exchange"]
 PC_NONE, PC_JACOBI, PC_CHEBYSHEV = 0, 1, 2
 
 
@@ -139,6 +140,8 @@ def load(path=None):
     lib.elas_dot.argtypes = [P, P, P, D]
     lib.elas_set_deterministic.restype = ctypes.c_int
     lib.elas_set_deterministic.argtypes = [P, ctypes.c_int]
+    lib.elas_set_peer_exchange.restype = ctypes.c_int
+    lib.elas_set_peer_exchange.argtypes = [P, ctypes.c_int]
     lib.elas_gmg_transfer.restype = ctypes.c_int
     lib.elas_gmg_transfer.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P]
     lib.elas_gmg_destroy.restype = None
@@ -329,6 +332,11 @@ def elas_dot(h, a, b):
     return out.value
 
 
+def elas_set_peer_exchange(h, on):
+    """Collective over the op's communicator: NVLink peer-store interface sums (on) or NCCL (off)."""
+    _check(load().elas_set_peer_exchange(h, 1 if on else 0), "elas_set_peer_exchange")
+
+
 def elas_set_deterministic(h, on):
     _check(load().elas_set_deterministic(h, int(bool(on))), "elas_set_deterministic")
 
@@ -473,6 +481,10 @@ class Operator:
 
     def set_deterministic(self, on=True):
         elas_set_deterministic(self.h, on)
+
+    def set_peer_exchange(self, on=True):
+        """NVLink peer-store interface sums instead of NCCL send/recv (collective; NCCL slab ops)."""
+        elas_set_peer_exchange(self.h, on)
 
     def chebyshev(self, order=3, alpha=0.1, beta=1.1, power_iters=10, v0=None, seed=0):
         c = Chebyshev(self, order, alpha, beta, power_iters, v0, seed)

@@ -3,7 +3,8 @@
 Checks the multi-GPU path of the library on real GPUs (A6, PAPER.md:169 P^T):
   1. elas_apply on NCCL slabs (interface planes summed by send/recv overlapped with the interior)
      == the single-GPU apply (<= 1e-14) and == the oracle (<= 1e-12, every row), replicated
-     interface planes bitwise equal on both ranks;
+     interface planes bitwise equal on both ranks; then the NVLink peer-store exchange
+     (elas_set_peer_exchange) bitwise equal to the NCCL one, over several epochs, timed A/B;
   2. the slab dot (elas_dot: owned-dof partials, ncclAllReduce) == the single-GPU dot;
   3. PCG with the slab Chebyshev smoother: iterates after 8 iterations == single GPU (<= 1e-10);
   4. one slab V-cycle (restriction with NCCL interface sums) == the single-GPU V-cycle (<= 1e-10);
@@ -92,6 +93,39 @@ def main():
         lam, mu = P.material_arrays()
         y_ref = oracle.apply(oracle.Mesh(P.vertex_array(), P.p, P.q, lam, mu, P.dirichlet_faces), P.x)
         assert rel(yg, y_ref) <= 1e-12, rel(yg, y_ref)
+
+    # ---- 1b. NVLink peer-store interface sum: bitwise equal to the NCCL exchange (ws >= 2) ---
+    if ws > 1:
+        op.set_deterministic(True)               # colored scatter: y bitwise reproducible run to run
+        op.apply(xl, yl)
+        y_nccl = yl.clone()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        for _ in range(10):
+            op.apply(xl, yl)
+        ev[1].record()
+        op.set_peer_exchange(True)
+        yp = torch.empty_like(yl)
+        for _ in range(3):                       # several epochs: flags, halo reuse
+            op.apply(xl, yp)
+            torch.cuda.synchronize()
+            assert torch.equal(yp, y_nccl), "peer-store exchange differs from NCCL"
+        ev[2].record()
+        for _ in range(10):
+            op.apply(xl, yp)
+        ev[3].record()
+        torch.cuda.synchronize()
+        assert torch.equal(yp, y_nccl)
+        t_nccl, t_peer = ev[0].elapsed_time(ev[1]) / 10, ev[2].elapsed_time(ev[3]) / 10
+        times = [None] * ws if rank == 0 else None
+        dist.gather_object((t_nccl, t_peer), times, dst=0)
+        if rank == 0:
+            print(f"apply ms per rank (NCCL exchange, peer store): {times}", flush=True)
+        _, parts = gather_slabs(P, yp.cpu().numpy(), K0, K1, rank, ws)
+        if rank == 0:
+            check_interfaces(parts, P.node_dims[0] * P.node_dims[1])   # replicas bitwise equal
+        op.set_peer_exchange(False)
+        op.set_deterministic(False)
 
     # ---- 2. slab dot -------------------------------------------------------------------------
     d = elas.elas_dot(op.h, xl, yl)

@@ -32,3 +32,19 @@ def test_nccl_slabs_vs_single_gpu_and_oracle(n):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=3600, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert f"MULTI OK n={n}" in r.stdout
+
+
+def test_peer_exchange_needs_nccl_slabs():
+    """elas_set_peer_exchange is collective over an NCCL communicator: single-GPU and
+    external-exchange ops are rejected with ELAS_EINVAL (runs on one GPU)."""
+    if gpus() < 1:
+        pytest.skip("no CUDA device")
+    import synth
+    from paper_2601_08374_b200 import elas
+    from paper_2601_08374_b200.elas import Operator
+    P = synth.make_problem("t", 2, 2, 4, 2, 4, seed=1)
+    for kw in ({}, {"rank": 0, "nranks": 2}):
+        op = Operator.from_problem(P, **kw)
+        with pytest.raises(elas.ElasError, match="NCCL-mode"):
+            op.set_peer_exchange(True)
+        op.close()
