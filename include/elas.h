@@ -308,6 +308,18 @@ int elas_pcg_gmg(elas_op* op, elas_gmg* g, const double* b, double* x, double rt
                  elas_solve_report* report, double* history);
 void elas_gmg_destroy(elas_gmg* g);   /* NULL-safe; synchronises */
 
+/* Debug build (lib/libelas_debug.so, compiled with ELAS_DEBUG=1): device-side bounds checks on
+ * every global gather / scatter / quadrature-data index of the apply kernels, the stand-in for
+ * compute-sanitizer (closed on this pool).  A failed check is counted (it does not trap).
+ * elas_debug_checks: synchronises nothing itself (call after cudaDeviceSynchronize); returns the
+ * number of failed checks since the last call (>= 0; negative ELAS_E* on a CUDA error), stores
+ * the source line of the first in *first_line (may be NULL) and resets the counters; selftest =
+ * 1 first runs one deliberately failing check (so the debug build returns >= 1).  In the release
+ * build the checks are compiled out and the count is always 0.
+ * elas_debug_build: 1 in the debug build, 0 otherwise. */
+int elas_debug_checks(int* first_line, int selftest);
+int elas_debug_build(void);
+
 /* Thread-local message describing the last error on this thread ("" if none). */
 const char* elas_last_error(void);
 

@@ -15,6 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, os.environ.get("ELAS_LIBNAME", "libelas.so"))
 EXTRA = [f"-D{d}" for d in os.environ.get("ELAS_DEFINES", "").split()]
+DEBUG_LIB = "libelas_debug.so"   # ELAS_DEBUG=1: device bounds checks (elas_debug_checks)
 ROOT = os.path.dirname(HERE)
 INCLUDE = os.path.join(ROOT, "include")
 
@@ -59,8 +60,21 @@ def _compile(src, obj, nccl_inc):
     return src, r.stderr
 
 
-def build(force=False, verbose=False):
-    """Compile every CUDA/C++ source for sm_100a and link lib/libelas.so (skips if up to date)."""
+def build(force=False, verbose=False, debug=False):
+    """Compile every CUDA/C++ source for sm_100a and link lib/libelas.so (skips if up to date).
+    debug=True: lib/libelas_debug.so with ELAS_DEBUG=1 (device bounds checks)."""
+    global LIB, EXTRA
+    if debug:
+        saved = LIB, EXTRA
+        LIB, EXTRA = os.path.join(LIBDIR, DEBUG_LIB), EXTRA + ["-DELAS_DEBUG=1"]
+        try:
+            return _build(force, verbose, "obj" + DEBUG_LIB)
+        finally:
+            LIB, EXTRA = saved
+    return _build(force, verbose, "obj" + os.environ.get("ELAS_LIBNAME", ""))
+
+
+def _build(force, verbose, objname):
     os.makedirs(LIBDIR, exist_ok=True)
     stamp = LIB + ".stamp"
     dig = _digest()
@@ -69,7 +83,7 @@ def build(force=False, verbose=False):
             if f.read().strip() == dig:
                 return LIB
     nccl_inc, nccl_lib = _nccl_paths()
-    objdir = os.path.join(LIBDIR, "obj" + os.environ.get("ELAS_LIBNAME", ""))
+    objdir = os.path.join(LIBDIR, objname)
     os.makedirs(objdir, exist_ok=True)
     srcs = _sources()
     objs = [os.path.join(objdir, s.rsplit(".", 1)[0] + ".o") for s in srcs]
@@ -97,4 +111,4 @@ def build(force=False, verbose=False):
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv)

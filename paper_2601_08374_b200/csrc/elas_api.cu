@@ -455,6 +455,25 @@ extern "C" {
 
 int elas_version(void) { return ELAS_VERSION; }
 
+int elas_debug_checks(int* first_line, int selftest) {
+  unsigned count = 0, line = 0;
+  if (selftest) {
+    CUDA_OR(elas::launch_dcheck_selftest(nullptr), "debug self-test launch");
+    CUDA_OR(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+  }
+  cudaError_t (*readers[])(unsigned*, unsigned*) = {
+      elas::dcheck_setup, elas::dcheck_p1t, elas::dcheck_tc,
+      elas::dcheck_eo_p1, elas::dcheck_eo_p2, elas::dcheck_eo_p3, elas::dcheck_eo_p4,
+      elas::dcheck_eo_p5, elas::dcheck_eo_p6, elas::dcheck_eo_p7, elas::dcheck_eo_p8,
+      elas::dcheck_simt_p1, elas::dcheck_simt_p2, elas::dcheck_simt_p3, elas::dcheck_simt_p4,
+      elas::dcheck_simt_p5, elas::dcheck_simt_p6, elas::dcheck_simt_p7, elas::dcheck_simt_p8};
+  for (auto rd : readers) CUDA_OR(rd(&count, &line), "debug check read");
+  if (first_line) *first_line = (int)line;
+  return (int)count;
+}
+
+int elas_debug_build(void) { return ELAS_DEBUG; }
+
 int elas_set_peer_exchange(elas_op* op, int on) {
   if (!op) { set_error("elas_set_peer_exchange: NULL op"); return ELAS_EINVAL; }
   if (op->nranks < 2 || op->external || !op->comm) {

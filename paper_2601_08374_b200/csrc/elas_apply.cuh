@@ -288,7 +288,10 @@ __global__ void __launch_bounds__(Cfg<P, Q>::NT, MinBlocks<P>::value)
     for (int k = 0; k < N; ++k) {
       const bool cons = bc && is_constrained(I, J, ez * P + k, s);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) u[c][k] = cons ? 0.0 : __ldg(x + c * s.nodes + base + k * plane);
+      for (int c = 0; c < 3; ++c) {
+        ELAS_DCHECK(base >= 0 && c * s.nodes + base + k * plane < 3 * s.nodes);
+        u[c][k] = cons ? 0.0 : __ldg(x + c * s.nodes + base + k * plane);
+      }
     }
     double* dst = sZ + el * C::ZE + j * N + i;
 #pragma unroll
@@ -497,7 +500,10 @@ __global__ void __launch_bounds__(Cfg<P, Q>::NT, MinBlocks<P>::value)
     for (int k = 0; k < N; ++k) {
       if (bc && is_constrained(I, J, ez * P + k, s)) continue;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) atomicAdd(y + c * s.nodes + base + k * plane, o[c][k]);
+      for (int c = 0; c < 3; ++c) {
+        ELAS_DCHECK(base >= 0 && c * s.nodes + base + k * plane < 3 * s.nodes);
+        atomicAdd(y + c * s.nodes + base + k * plane, o[c][k]);
+      }
     }
   }
 }
@@ -530,6 +536,7 @@ void info_pq(ApplyLaunch* info) {
 
 // Instantiate the two quadrature variants q = p+1, p+2 of one degree P.
 #define ELAS_DEFINE_DEGREE(P)                                                                   \
+  ELAS_DCHECK_READER(dcheck_simt_p##P)                                                          \
   namespace elas {                                                                              \
   cudaError_t apply_info_p##P(int q, ApplyLaunch* info) {                                       \
     if (q == P + 1) info_pq<P, P + 1>(info);                                                    \

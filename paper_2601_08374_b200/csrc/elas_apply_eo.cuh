@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
       for (int k = 0; k < N; ++k)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
+          ELAS_DCHECK((int64_t)(xb - x) + c * nodes32 + k * plane32 < 3 * s.nodes && xb >= x);
           double v;
           asm("ld.global.nc.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(xb + (c * nodes32 + k * plane32)));
           u[c][k] = (T)v;
@@ -395,7 +396,10 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
       for (int k = 0; k < N; ++k) {
         const bool cons = bc && is_constrained(I, J, ez * P + k, s);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) u[c][k] = cons ? T(0) : (T)__ldg(x + c * s.nodes + base + k * plane);
+        for (int c = 0; c < 3; ++c) {
+          ELAS_DCHECK(base >= 0 && c * s.nodes + base + k * plane < 3 * s.nodes);
+          u[c][k] = cons ? T(0) : (T)__ldg(x + c * s.nodes + base + k * plane);
+        }
       }
       }
     }
@@ -664,6 +668,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
         }
       }
     }
+    ELAS_DCHECK(e >= 0 && e < (int64_t)s.nx * s.ny * s.nz && xex < s.nx && xey < s.ny && xez < s.nz);
     const T r = (T)__ldg(rr + e);
     const T* qp = STG ? sQ + el * C::QDE + L : qd + e * (int64_t)C::QDE + L;
     // geometry on the fly: per-line constants
@@ -909,6 +914,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
     }
     const int I = ex * P + i, J = ey * P + j;
     const int64_t base = I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
+    ELAS_DCHECK(base >= 0 && 2 * s.nodes + base + (N - 1) * plane < 3 * s.nodes && I < s.Nx && J < s.Ny);
 #pragma unroll
     for (int k = 0; k < NE; ++k) {
       const bool kmid = (N & 1) && k == NH;
@@ -994,6 +1000,7 @@ cudaError_t upload_eo_pq(const double* fold) {
 }  // namespace elas
 
 #define ELAS_DEFINE_DEGREE_EO(P)                                                                \
+  ELAS_DCHECK_READER(dcheck_eo_p##P)                                                            \
   namespace elas {                                                                              \
   cudaError_t apply_eo_info_p##P(int q, int fp32, ApplyLaunch* info) {                          \
     if (q == P + 1) fp32 ? info_eo_pq<P, P + 1, float>(info) : info_eo_pq<P, P + 1, double>(info); \

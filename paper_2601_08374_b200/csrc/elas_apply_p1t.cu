@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(NT, ELAS_P1T_MINB)
       for (int i = 0; i < 2; ++i) {
         const bool z = bc && cons(ex + i, ey + j, ez + k, s);
         const int64_t o = base + i + (int64_t)s.Nx * j + plane * k;
+        ELAS_DCHECK(o >= 0 && 2 * s.nodes + o < 3 * s.nodes);
 #pragma unroll
         for (int c = 0; c < 3; ++c) su[(c * 8 + k * 4 + j * 2 + i) * NT + threadIdx.x] = z ? 0.0 : __ldg(x + c * s.nodes + o);
       }
@@ -229,6 +230,7 @@ __global__ void __launch_bounds__(NT, ELAS_P1T_MINB)
       for (int i = 0; i < 2; ++i) {
         if (bc && cons(ex + i, ey + j, ez + k, s)) continue;
         const int64_t o = base + i + (int64_t)s.Nx * j + plane * k;
+        ELAS_DCHECK(o >= 0 && 2 * s.nodes + o < 3 * s.nodes);
 #pragma unroll
         for (int c = 0; c < 3; ++c) atomicAdd(y + c * s.nodes + o, out[c][k][j][i]);
       }
@@ -261,3 +263,5 @@ cudaError_t apply_p1t_launch(int q, const Slab& s, const double* x, double* y, c
 }
 
 }  // namespace elas
+
+ELAS_DCHECK_READER(dcheck_p1t)

@@ -27,3 +27,5 @@ cudaError_t apply_tc_launch(const Slab& s, const double* x, double* y, const dou
 }
 
 }  // namespace elas
+
+ELAS_DCHECK_READER(dcheck_tc)

@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(32 * WPE * EPC, 1)
           int c, j, k;
           fibre(16 * (WPE * u + half) + g + 8 * h, c, j, k);
           const double* src = x + c * s.nodes + ebase + (int64_t)s.Nx * j + plane * k;
+          ELAS_DCHECK(src >= x && (src - x) + N - 1 < 3 * s.nodes);
           double lo = __ldg(src + jlo), hi = __ldg(src + jhi);
           if (bc) {
             if (cons(I0 + jlo, J0 + j, K0 + k, s)) lo = 0.0;
@@ -489,6 +490,7 @@ __global__ void __launch_bounds__(32 * WPE * EPC, 1)
           const int i = 2 * t + uu;
           if (i >= N) continue;
           if (bc && cons(I0 + i, J0 + jj[h], K0 + kk[h], s)) continue;
+          ELAS_DCHECK(dst >= y && (dst - y) + i < 3 * s.nodes);
           atomicAdd(dst + i, o[2 * h + uu]);
         }
       }

@@ -8,6 +8,47 @@
 
 #include "../../include/elas.h"
 
+// Debug build (ELAS_DEBUG=1, lib/libelas_debug.so): device-side bounds checks on every global
+// gather/scatter/quadrature-data index of the apply kernels -- the substitute for
+// compute-sanitizer, which is closed on this pool.  A failed check does not trap (a trapped
+// kernel can take the GPU down): it counts itself and records its source line in a per-TU
+// device word that elas_debug_checks() reads and resets.  In the release build the checks
+// compile to nothing.
+#ifndef ELAS_DEBUG
+#define ELAS_DEBUG 0
+#endif
+#if defined(__CUDACC__)
+namespace elas {
+namespace {
+__device__ unsigned int g_dcheck[2];   // [0] failed checks, [1] source line of the first failure
+}  // namespace
+}  // namespace elas
+#if ELAS_DEBUG
+#define ELAS_DCHECK(cond)                                                                \
+  do {                                                                                   \
+    if (!(cond)) {                                                                       \
+      if (atomicAdd(&::elas::g_dcheck[0], 1u) == 0u) ::elas::g_dcheck[1] = __LINE__;     \
+    }                                                                                    \
+  } while (0)
+#else
+#define ELAS_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+// host reader of this translation unit's check words: adds the count, keeps the first line, resets
+#define ELAS_DCHECK_READER(NAME)                                                           \
+  namespace elas {                                                                         \
+  cudaError_t NAME(unsigned* count, unsigned* line) {                                      \
+    unsigned h[2] = {0, 0}, z[2] = {0, 0};                                                 \
+    cudaError_t e = cudaMemcpyFromSymbol(h, g_dcheck, sizeof(h));                          \
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_dcheck, z, sizeof(z));                  \
+    if (h[0] && !*count) *line = h[1];                                                     \
+    *count += h[0];                                                                        \
+    return e;                                                                              \
+  }                                                                                        \
+  }
+#endif
+
 namespace elas {
 
 // Everything a kernel needs to address one rank's slab (all LOCAL indices).
@@ -111,6 +152,15 @@ cudaError_t launch_plane_add(const Slab& s, int which_plane, double* y, const do
 // one thread stores value into a (possibly peer, IPC-mapped) flag with release semantics
 cudaError_t launch_wait_flag(const unsigned long long* flag, unsigned long long target, cudaStream_t st);
 cudaError_t launch_signal_flag(unsigned long long* flag, unsigned long long value, cudaStream_t st);
+// debug build: the per-translation-unit readers of the device check words (ELAS_DCHECK_READER)
+cudaError_t launch_dcheck_selftest(cudaStream_t st);
+#define ELAS_DCHECK_DECL(NAME) cudaError_t NAME(unsigned* count, unsigned* line);
+ELAS_DCHECK_DECL(dcheck_setup) ELAS_DCHECK_DECL(dcheck_p1t) ELAS_DCHECK_DECL(dcheck_tc)
+ELAS_DCHECK_DECL(dcheck_eo_p1) ELAS_DCHECK_DECL(dcheck_eo_p2) ELAS_DCHECK_DECL(dcheck_eo_p3) ELAS_DCHECK_DECL(dcheck_eo_p4)
+ELAS_DCHECK_DECL(dcheck_eo_p5) ELAS_DCHECK_DECL(dcheck_eo_p6) ELAS_DCHECK_DECL(dcheck_eo_p7) ELAS_DCHECK_DECL(dcheck_eo_p8)
+ELAS_DCHECK_DECL(dcheck_simt_p1) ELAS_DCHECK_DECL(dcheck_simt_p2) ELAS_DCHECK_DECL(dcheck_simt_p3) ELAS_DCHECK_DECL(dcheck_simt_p4)
+ELAS_DCHECK_DECL(dcheck_simt_p5) ELAS_DCHECK_DECL(dcheck_simt_p6) ELAS_DCHECK_DECL(dcheck_simt_p7) ELAS_DCHECK_DECL(dcheck_simt_p8)
+#undef ELAS_DCHECK_DECL
 
 // error helpers
 void set_error(const std::string& msg);

@@ -141,9 +141,13 @@ __global__ void plane_add_kernel(Slab s, int K, double* __restrict__ y, const do
     const int I = (int)(pidx % s.Nx), J = (int)(pidx / s.Nx);
     if (s.faces && constrained_node(I, J, K, s)) continue;
     double* dst = y + c * s.nodes + (int64_t)K * plane + pidx;
+    ELAS_DCHECK(K >= 0 && K < s.Nz && c * s.nodes + (int64_t)K * plane + pidx < 3 * s.nodes);
     *dst = *dst + halo[t];
   }
 }
+
+// debug-build self-test: one deliberately failed check (elas_debug_checks(..., selftest = 1))
+__global__ void dcheck_selftest_kernel(int v) { ELAS_DCHECK(v == 0); }
 
 __global__ void wait_flag_kernel(const unsigned long long* flag, unsigned long long target) {
   unsigned long long v;
@@ -277,4 +281,11 @@ cudaError_t launch_signal_flag(unsigned long long* flag, unsigned long long valu
   return cudaGetLastError();
 }
 
+cudaError_t launch_dcheck_selftest(cudaStream_t st) {
+  dcheck_selftest_kernel<<<1, 1, 0, st>>>(1);
+  return cudaGetLastError();
+}
+
 }  // namespace elas
+
+ELAS_DCHECK_READER(dcheck_setup)

@@ -33,7 +33,7 @@ EXPORTED = ["elas_create", "elas_apply", "elas_apply_host", "elas_interface_add"
             "elas_cheb_destroy", "elas_pcg", "elas_gmg_create", "elas_gmg_level_op", "elas_gmg_levels",
             "elas_gmg_set_stream", "elas_gmg_apply", "elas_pcg_gmg", "elas_gmg_destroy", "elas_gmg_transfer",
             "elas_set_deterministic", "elas_dot", "elas_create_aniso", "elas_apply_add",
-            "elas_set_peer_exchange"]
+            "elas_set_peer_exchange", "elas_debug_checks", "elas_debug_build"]
 PC_NONE, PC_JACOBI, PC_CHEBYSHEV = 0, 1, 2
 
 
@@ -142,6 +142,10 @@ def load(path=None):
     lib.elas_set_deterministic.argtypes = [P, ctypes.c_int]
     lib.elas_set_peer_exchange.restype = ctypes.c_int
     lib.elas_set_peer_exchange.argtypes = [P, ctypes.c_int]
+    lib.elas_debug_checks.restype = ctypes.c_int
+    lib.elas_debug_checks.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int]
+    lib.elas_debug_build.restype = ctypes.c_int
+    lib.elas_debug_build.argtypes = []
     lib.elas_gmg_transfer.restype = ctypes.c_int
     lib.elas_gmg_transfer.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P]
     lib.elas_gmg_destroy.restype = None
@@ -330,6 +334,19 @@ def elas_dot(h, a, b):
     out = ctypes.c_double(0.0)
     _check(load().elas_dot(h, _ptr(a), _ptr(b), ctypes.byref(out)), "elas_dot")
     return out.value
+
+
+def elas_debug_checks(selftest=False):
+    """(failed device bounds checks since the last call, source line of the first); debug build."""
+    line = ctypes.c_int(0)
+    n = load().elas_debug_checks(ctypes.byref(line), 1 if selftest else 0)
+    if n < 0:
+        raise ElasError(n, f"elas_debug_checks: {elas_last_error()}")
+    return n, line.value
+
+
+def elas_debug_build():
+    return bool(load().elas_debug_build())
 
 
 def elas_set_peer_exchange(h, on):
