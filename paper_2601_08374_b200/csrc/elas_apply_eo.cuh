@@ -122,7 +122,10 @@ using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEOT<P, T>::value, (int)sizeof(T), 
 // [R][9][NT] so both the copies and the reads are contiguous across a warp.
 // measured (tools/ab_libs.sh, config 4): an aliased ring of 4 points helps at p >= 6
 // (p6 29.9 -> 30.7, p8 27.5 -> 28.8 GDoF/s); at p <= 5 the Z buffer holds at most 2 slots per
-// thread and the one-point register prefetch is as good or better.
+// thread and the one-point register prefetch is as good or better.  Round 2 (96-thread CTAs and the
+// 32-bit gather at p7): the one-point register prefetch beats the ring for the FP64 p7 instance
+// (24.5 -> 25.05), ties at p6 (33.62 / 33.68) and loses at p8 (30.39 -> 29.78) and for FP32 p7
+// (48.4 -> 40.0).
 #ifndef ELAS_QD_RING
 #define ELAS_QD_RING (P >= 6 ? 4 : 0)
 #endif
@@ -138,7 +141,8 @@ struct RingEO {
   // barrier); a dedicated ring costs occupancy and lost everywhere
   static constexpr bool ALIAS = true;
   static constexpr int RMAX = ALIAS ? (C::EB * C::ZE) / (9 * C::NT) : 16;
-  static constexpr int R0 = ELAS_QD_RING < RMAX ? ELAS_QD_RING : RMAX;
+  static constexpr int WANT = (WB == 8 && P == 7) ? 0 : ELAS_QD_RING;
+  static constexpr int R0 = WANT < RMAX ? WANT : RMAX;
   static constexpr int R = R0 >= 2 ? R0 : 0;
   static constexpr bool STAGE = C::STAGE_QD && R == 0 && StageEO<P>::value;  // whole-CTA TMA staging
   static constexpr int OFF = ALIAS ? C::TAB : (C::TAB + C::EB * (C::ZE + C::YE) + C::AL - 1) & ~(C::AL - 1);
