@@ -6,7 +6,11 @@ KEYS = {"kernel": "Kernel Name", "ms": "gpu__time_duration.sum", "regs": "launch
         "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "issue_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "dram_read": "dram__bytes_read.sum", "dram_write": "dram__bytes_write.sum",
-        "smem_wavefronts_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"}
+        "smem_wavefronts_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "smem_bank_conflicts": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "inst_executed": "smsp__inst_executed.sum", "grid": "launch__grid_size",
+        "l2_hit_pct": "lts__t_sector_hit_rate.pct"}
 out = {}
 for p in range(1, 9):
     raw = subprocess.run(["ncu", "-i", f"gpurun_out/ncu_allp_{p}.ncu-rep", "--page", "raw", "--csv"],
@@ -18,4 +22,12 @@ for p in range(1, 9):
     hdr, units, vals = rows[0], rows[1], rows[2]
     d, u = dict(zip(hdr, vals)), dict(zip(hdr, units))
     out[str(p)] = {k: (d.get(m, "") + (" " + u.get(m, "") if u.get(m) else "")).strip() for k, m in KEYS.items()}
+    st = {}
+    for h, v in d.items():   # warp-state stall samples (smsp__pcsamp_warps_issue_stalled_*)
+        if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued"):
+            try:
+                st[h[len("smsp__pcsamp_warps_issue_stalled_"):]] = int(float(v.replace(",", "")))
+            except ValueError:
+                pass
+    out[str(p)]["stalls_top"] = dict(sorted(st.items(), key=lambda kv: -kv[1])[:6])
 json.dump(out, sys.stdout, indent=1)
