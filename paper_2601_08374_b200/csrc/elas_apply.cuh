@@ -67,23 +67,30 @@ constexpr int pick_SA(int N, int Q, int G = 16) {
   return best;
 }
 
-// a2-stride of the Y buffer: stage X lanes are lines L = a3 + Q a2 (a3 fast)
-constexpr int pick_S2(int N, int Q, int G = 16) {
-  int best = Q * N, best_cost = 1 << 30;
-  for (int S2 = Q * N; S2 < Q * N + G; ++S2) {
+// a2-stride of the Y buffer: stage X lanes are lines L = a3 + Q a2 (a3 fast), a3-stride LN
+constexpr int pick_S2(int N, int Q, int LN, int G = 16) {
+  int best = Q * LN, best_cost = 1 << 30;
+  for (int S2 = Q * LN; S2 < Q * LN + G; ++S2) {
     int addr[512] = {0};
     int n = 0;
     for (int a2 = 0; a2 < Q; ++a2)
-      for (int a3 = 0; a3 < Q; ++a3) addr[n++] = a2 * S2 + a3 * N;
+      for (int a3 = 0; a3 < Q; ++a3) addr[n++] = a2 * S2 + a3 * LN;
     int c = halfwarp_cost(addr, n, G);
     if (c < best_cost) { best_cost = c; best = S2; }
   }
   return best;
 }
 
+// a3-stride (line stride) of the Y buffer.  Stage X reads and writes whole x-lines, one lane per
+// line (a3 fast), so an even node count N as the stride puts the lanes of a half-warp on few
+// banks: at p = 7 (N = 8) 9 lanes share 2 double-word banks and 76 % of that stage's shared
+// wavefronts are conflicts (ncu, round 2; tools/smem_by_line.py).  LNO: the next odd stride
+// instead (stage Y/Yt then pay a 2-way conflict on one bank per half-warp).
+constexpr int pick_LN(int N, int LNO) { return LNO ? (N | 1) : N; }
+
 // element strides of the Z and Y buffers: at low order one warp spans several elements, so
 // pad the element strides to minimise conflicts over whole warps of every stage's pattern
-constexpr int elem_pattern_cost(int N, int Q, int SA, int S2, int ZE, int YE, int NT, int G = 16) {
+constexpr int elem_pattern_cost(int N, int Q, int SA, int S2, int LN, int ZE, int YE, int NT, int G = 16) {
   int total = 0;
   int addr[512] = {0};
   const int lanes = NT < 512 ? NT : 512;
@@ -93,27 +100,27 @@ constexpr int elem_pattern_cost(int N, int Q, int SA, int S2, int ZE, int YE, in
   // stage Y / Yt: Z buffer and Y buffer, lanes (i, a3, el)
   for (int w = 0; w < lanes; ++w) addr[w] = (w / (N * Q)) * ZE + ((w / N) % Q) * SA + w % N;
   total += halfwarp_cost(addr, lanes, G);
-  for (int w = 0; w < lanes; ++w) addr[w] = (w / (N * Q)) * YE + ((w / N) % Q) * N + w % N;
+  for (int w = 0; w < lanes; ++w) addr[w] = (w / (N * Q)) * YE + ((w / N) % Q) * LN + w % N;
   total += halfwarp_cost(addr, lanes, G);
   // stage X: Y buffer, lanes (a3, a2, el)
-  for (int w = 0; w < lanes; ++w) addr[w] = (w / (Q * Q)) * YE + ((w / Q) % Q) * S2 + (w % Q) * N;
+  for (int w = 0; w < lanes; ++w) addr[w] = (w / (Q * Q)) * YE + ((w / Q) % Q) * S2 + (w % Q) * LN;
   total += halfwarp_cost(addr, lanes, G);
   return total;
 }
 
-constexpr int pick_ZE(int N, int Q, int SA, int S2, int ZE0, int YE0, int NT, int G = 16) {
+constexpr int pick_ZE(int N, int Q, int SA, int S2, int LN, int ZE0, int YE0, int NT, int G = 16) {
   int best = ZE0, bc = 1 << 30;
   for (int p = 0; p < G; ++p) {
-    const int c = elem_pattern_cost(N, Q, SA, S2, ZE0 + p, YE0, NT, G);
+    const int c = elem_pattern_cost(N, Q, SA, S2, LN, ZE0 + p, YE0, NT, G);
     if (c < bc) { bc = c; best = ZE0 + p; }
   }
   return best;
 }
 
-constexpr int pick_YE(int N, int Q, int SA, int S2, int ZE, int YE0, int NT, int G = 16) {
+constexpr int pick_YE(int N, int Q, int SA, int S2, int LN, int ZE, int YE0, int NT, int G = 16) {
   int best = YE0, bc = 1 << 30;
   for (int p = 0; p < G; ++p) {
-    const int c = elem_pattern_cost(N, Q, SA, S2, ZE, YE0 + p, NT, G);
+    const int c = elem_pattern_cost(N, Q, SA, S2, LN, ZE, YE0 + p, NT, G);
     if (c < bc) { bc = c; best = YE0 + p; }
   }
   return best;
@@ -143,7 +150,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 constexpr int qd_stride_words(int q, int WB) { return WB == 8 ? (9 * q * q * q + 1) & ~1 : (9 * q * q * q + 3) & ~3; }
 
 // PAD = 0: unpadded tiles (minimal shared memory, bank conflicts accepted)
-template <int P, int Q, int TABSZ = 2 * Q * (P + 1), int NTHR = ELAS_NT, int WB = 8, int PAD = 1>
+template <int P, int Q, int TABSZ = 2 * Q * (P + 1), int NTHR = ELAS_NT, int WB = 8, int PAD = 1, int LNO = 0>
 struct Cfg {
   static constexpr int N = P + 1;
   static constexpr int NT = NTHR;
@@ -152,11 +159,12 @@ struct Cfg {
   static constexpr int SA = PAD ? pick_SA(N, Q, G) : N * N;
   static constexpr int ZV = Q * SA;        // variant stride (Zb | Zd)
   static constexpr int ZC = 2 * ZV;        // component stride
-  static constexpr int S2 = PAD ? pick_S2(N, Q, G) : Q * N;
-  static constexpr int ZE = PAD ? pick_ZE(N, Q, SA, S2, 3 * ZC, 9 * Q * S2, NT, G) : 3 * ZC;  // element stride
+  static constexpr int LN = pick_LN(N, LNO);  // a3-stride (x-line) of the Y buffer
+  static constexpr int S2 = PAD ? pick_S2(N, Q, LN, G) : Q * LN;
+  static constexpr int ZE = PAD ? pick_ZE(N, Q, SA, S2, LN, 3 * ZC, 9 * Q * S2, NT, G) : 3 * ZC;  // element stride
   static constexpr int YV = Q * S2;        // variant stride (Y0 | Y1 | Y2)
   static constexpr int YC = 3 * YV;        // component stride
-  static constexpr int YE = PAD ? pick_YE(N, Q, SA, S2, ZE, 3 * YC, NT, G) : 3 * YC;  // element stride
+  static constexpr int YE = PAD ? pick_YE(N, Q, SA, S2, LN, ZE, 3 * YC, NT, G) : 3 * YC;  // element stride
   static constexpr int TAB = (TABSZ + AL - 1) & ~(AL - 1);  // coefficient tables (B then D, or folded)
   // elements per CTA: enough x-lines for every thread in stage X; at low order also enough
   // z-columns (N^2 per element) to keep every thread busy in stages Z and Zt.
@@ -327,7 +335,7 @@ __global__ void __launch_bounds__(Cfg<P, Q>::NT, MinBlocks<P>::value)
         zb[c][j] = src[c * C::ZC + j * N];
         zd[c][j] = src[c * C::ZC + C::ZV + j * N];
       }
-    double* dst = sY + el * C::YE + a3 * N + i;
+    double* dst = sY + el * C::YE + a3 * C::LN + i;
 #pragma unroll
     for (int a2 = 0; a2 < Q; ++a2) {
       double y0[3] = {0, 0, 0}, y1[3] = {0, 0, 0}, y2[3] = {0, 0, 0};
@@ -362,7 +370,7 @@ __global__ void __launch_bounds__(Cfg<P, Q>::NT, MinBlocks<P>::value)
     const int L = w % (Q * Q), el = w / (Q * Q);
     const int a3 = L % Q, a2 = L / Q;
     const int64_t e = e0 + el;
-    double* line = sY + el * C::YE + a2 * C::S2 + a3 * N;
+    double* line = sY + el * C::YE + a2 * C::S2 + a3 * C::LN;
     double g[3][3][Q];
 #pragma unroll
     for (int v = 0; v < 3; ++v) {
@@ -432,7 +440,7 @@ __global__ void __launch_bounds__(Cfg<P, Q>::NT, MinBlocks<P>::value)
   // ---------------- Stage Yt: transposed contraction in y ------------------------------
   for (int w = tid; w < ne * Q * N; w += NT) {
     const int i = w % N, a3 = (w / N) % Q, el = w / (N * Q);
-    const double* src = sY + el * C::YE + a3 * N + i;
+    const double* src = sY + el * C::YE + a3 * C::LN + i;
     double wb[3][N], wd[3][N];
 #pragma unroll
     for (int c = 0; c < 3; ++c)

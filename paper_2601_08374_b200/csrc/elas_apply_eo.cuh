@@ -112,8 +112,17 @@ template <int P> struct PersistEO { static constexpr bool value = P == 5; };
 #endif
 template <int P> struct G32EO { static constexpr bool value = ((ELAS_EO_G32_MASK >> P) & 1) != 0; };
 
+// Odd Y-buffer line stride (Cfg LNO, pick_LN) per degree (bit p); measured (config 4, GDoF/s):
+// FP64 p7 25.0 -> 27.2, FP32 p7 49.0 -> 49.2; p5 30.5 -> 29.2 and p3 23.9 -> 23.7 lose (their
+// x-line conflicts are 2-way, the new stage-Y conflict costs more).  Walking stages Y/Yt a3-fast
+// to keep them conflict-free at the odd stride measured 27.0 at p7 (rejected).
+#ifndef ELAS_EO_LNO_MASK
+#define ELAS_EO_LNO_MASK (1 << 7)
+#endif
+template <int P> struct LnoEO { static constexpr int value = (ELAS_EO_LNO_MASK >> P) & 1; };
+
 template <int P, int Q, typename T = double>
-using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEOT<P, T>::value, (int)sizeof(T), 1>;
+using CfgEO = Cfg<P, Q, 2 * Fold<P, Q>::TS, NtEOT<P, T>::value, (int)sizeof(T), 1, LnoEO<P>::value>;
 
 // Quadrature-data ring (ELAS_QD_RING = R > 0): every stage-X thread owns one x-line (EB q^2 <=
 // NT), so it streams ITS line's 9 values per point into its own shared-memory slots with
@@ -564,7 +573,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
       fold_in<N, NE, NHX>(zb, bp, bm);
       fold_in<N, NE, NHX>(zd, dp, dm);
     }
-    T* dst = sY + el * C::YE + a3 * N + i;
+    T* dst = sY + el * C::YE + a3 * C::LN + i;
 #pragma unroll
     for (int a2 = 0; a2 < QE; ++a2) {
       const bool mid = (Q & 1) && a2 == QH;
@@ -630,7 +639,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
     const int a3 = L % Q, a2 = L / Q;
     int xex, xey, xez;
     const int64_t e = elem_coords<COLORED>(cm, s, e0 + el, xex, xey, xez);
-    T* line = sY + el * C::YE + a2 * C::S2 + a3 * N;
+    T* line = sY + el * C::YE + a2 * C::S2 + a3 * C::LN;
     T g[3][3][Q];
 #pragma unroll
     for (int v = 0; v < 3; ++v) {
@@ -796,7 +805,7 @@ __global__ void __launch_bounds__(CfgEO<P, Q, T>::NT, sizeof(T) == 4 ? MinbEO32<
   // ---------------- Stage Yt: folded transposed contraction in y ------------------------
   for (int w = tid; w < ne * Q * N; w += NT) {
     const int i = w % N, a3 = (w / N) % Q, el = w / (N * Q);
-    const T* src = sY + el * C::YE + a3 * N + i;
+    const T* src = sY + el * C::YE + a3 * C::LN + i;
     // wb = By^T V0 + Dy^T V1, wd = By^T V2 ; X/Y sums per node pair (j, n-1-j)
     T bX[3][NE], bY[3][NE], dX[3][NE], dY[3][NE];
 #pragma unroll
