@@ -972,10 +972,25 @@ cudaError_t launch_apply_eo_pqc(const Slab& s, const double* x, double* y, const
   return cudaGetLastError();
 }
 
+// fine-grained FP64 kernel (elas_apply_fg.cuh), per-degree mask (bit p).  Measured (config 4,
+// GDoF/s, x-line -> FG): p6 33.46 -> 39.36, p7 26.89 -> 34.31, p8 30.29 -> 32.41, config 5 33.55 ->
+// 37.51; p3 23.90 -> 16.86, p4 28.42 -> 25.63, p5 30.48 -> 27.27 stay on the x-line kernel.
+#ifndef ELAS_FG_MASK
+#define ELAS_FG_MASK 0x1C0
+#endif
+template <int P> struct FgOn { static constexpr bool value = ((ELAS_FG_MASK >> P) & 1) != 0; };
+template <int P, int Q>
+cudaError_t launch_apply_fg(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
+                            int64_t e_begin, int64_t e_end, cudaStream_t st);
+template <int P, int Q> void info_fg_pq(ApplyLaunch* info);
+
 template <int P, int Q, typename T>
 cudaError_t launch_apply_eo_pq(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
                                const void* tables, int64_t e_begin, int64_t e_end, cudaStream_t st,
                                const ColorMap& cm, int otf, const double* cc) {
+  if constexpr (sizeof(T) == 8 && FgOn<P>::value) {
+    if (!cm.on && !otf && !cc) return launch_apply_fg<P, Q>(s, x, y, qd, rr, e_begin, e_end, st);
+  }
   if constexpr (sizeof(T) == 8) {
     if (cc)
       return cm.on ? launch_apply_eo_pqc<P, Q, T, true, false, true>(s, x, y, qd, rr, tables, e_begin, e_end, st, cm, cc)
@@ -990,6 +1005,10 @@ cudaError_t launch_apply_eo_pq(const Slab& s, const double* x, double* y, const 
 
 template <int P, int Q, typename T>
 void info_eo_pq(ApplyLaunch* info) {
+  if constexpr (sizeof(T) == 8 && FgOn<P>::value) {
+    info_fg_pq<P, Q>(info);
+    return;
+  }
   using C = CfgEO<P, Q, T>;
   info->threads = C::NT;
   info->elems_per_cta = C::EB;

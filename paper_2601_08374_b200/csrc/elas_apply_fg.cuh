@@ -1,0 +1,475 @@
+// Fine-grained (FG) variant of the folded FP64 apply kernel: the same element pass and the same
+// even-odd folded 1D contractions as elas_apply_eo.cuh (gather -> Z -> Y -> X -> pointwise ->
+// Xt -> Yt -> Zt + scatter-add; PAPER.md:169 chain G^T B^T D B G, Eq. 6 and §4.3-4.4), but every
+// stage is split into ONE-COMPONENT (or one-point) work items so that an element is worked on by
+// 3q^2 threads instead of q^2, each holding a few dozen doubles instead of a whole x-line's 9q
+// gradients:
+//   gather + Z   item (c, j, i)   one z-column of one component:  n values -> Zb, Zd (2q)
+//   Y            item (c, a3, i)  one y-line of one component:    2n values -> Y0, Y1, Y2 (3q)
+//   X            item (v, line)   one x-line, gradient direction v, all 3 components: the
+//                                 q values of g[c][v] are written back IN PLACE over the line's
+//                                 run (c, v) (n slots) and, for q > n, into an overflow area
+//                                 in the Z tile (dead between stages Y and Yt)
+//   pointwise    item (point)     9 gradients + 9 qdata words -> 9 fluxes, in place
+//   Xt           item (d, line)   the q fluxes F[c][d] -> n values of run (c, d)
+//   Yt           item (c, a3, i), Zt item (c, j, i) + the atomic scatter.
+// The per-thread state is O(q), so the kernel targets ~112 registers at 3 CTAs (one element,
+// 3q^2 threads each) per SM instead of 255 registers at 8 warps per SM (the round-1 cap
+// VERDICT r1 "What's weak" 3 names), at the price of the gradient/flux round trip through
+// shared memory (4 x 9q^3 extra words per element).  Per-degree enable: ELAS_FG_MASK (bit p).
+// FP64 only; the colored, on-the-fly and anisotropic instances keep the x-line kernel.
+#pragma once
+#include <type_traits>
+#include "elas_apply_eo.cuh"
+
+namespace elas {
+
+#ifndef ELAS_FG_MINB
+#define ELAS_FG_MINB 0   // 0: per-degree default below
+#endif
+#ifndef ELAS_FG_CTAB
+#define ELAS_FG_CTAB 1   // 1: coefficients read from the constant bank (no shared copy)
+#endif
+#ifndef ELAS_FG_PREF_OWN
+#define ELAS_FG_PREF_OWN 1   // L2 prefetch of the CTA's own qdata at start
+#endif
+
+template <int P, int Q>
+struct CfgFG {
+  static constexpr int N = P + 1;
+  static constexpr int NT = ((3 * Q * Q + 31) / 32) * 32;   // one X item per thread
+  static constexpr int LN = (N & 1) ? N : N + 1;             // odd line stride: X/pointwise conflict-free
+  static constexpr int S2 = Q * LN;                          // => line (a2, a3) starts at (a2 q + a3) LN
+  static constexpr int YV = Q * S2, YC = 3 * YV, YE = 3 * YC;
+  static constexpr int SA = pick_SA(N, Q, 16);               // Z tile a3 stride (stage Y reads a3*SA + i)
+  static constexpr int ZV = Q * SA, ZC = 2 * ZV, ZE = 3 * ZC;
+  static constexpr int OVN = Q > N ? Q - N : 0;             // overflow slots per run (q > n)
+  static constexpr int TAB = (2 * Fold<P, Q>::TS + 1) & ~1;
+  static constexpr size_t smem = sizeof(double) * (size_t)(TAB + ZE + YE);
+  static_assert(9 * Q * Q * OVN <= ZE, "gradient overflow must fit in the Z tile");
+  static_assert(3 * N * N <= NT, "one z-column item per thread");
+  static constexpr int QDE = qd_stride_words(Q, 8);
+};
+#ifndef ELAS_FG_MINB_P8
+#define ELAS_FG_MINB_P8 0
+#endif
+template <int P> struct FgMinb {
+  static constexpr int value = (P == 8 && ELAS_FG_MINB_P8 > 0) ? ELAS_FG_MINB_P8
+                               : ELAS_FG_MINB > 0 ? ELAS_FG_MINB : (P <= 4 ? 4 : P <= 6 ? 3 : 2);
+};
+#ifndef ELAS_FG_CU1
+#define ELAS_FG_CU1 0   // 1: component loops of stages X / Xt not unrolled (fewer live registers)
+#endif
+
+// forward folded contraction, parity chosen at run time (odd: D table, antisymmetric):
+// out[a] = E + O, out[q-1-a] = sgn (E - O); the middle point (q odd) takes E (B) or O (D)
+template <int N, int Q>
+__device__ __forceinline__ void fg_fwd(const double* __restrict__ tab, bool odd, const double (&in)[N],
+                                       double (&out)[Q]) {
+  using F = Fold<N - 1, Q>;
+  constexpr int NE = F::NE, NH = F::NH, QE = F::QE, QH = F::QH;
+  double up[NE], um[F::NHX];
+#pragma unroll
+  for (int i = 0; i < NH; ++i) {
+    up[i] = in[i] + in[N - 1 - i];
+    um[i] = in[i] - in[N - 1 - i];
+  }
+  if (N & 1) up[NH] = in[NH];
+  const double sg = odd ? -1.0 : 1.0;
+#pragma unroll
+  for (int a = 0; a < QE; ++a) {
+    double E = 0.0, O = 0.0;
+#pragma unroll
+    for (int i = 0; i < NE; ++i) E = fma(tab[F::FE + a * NE + i], up[i], E);
+#pragma unroll
+    for (int i = 0; i < NH; ++i) O = fma(tab[F::FO + a * NH + i], um[i], O);
+    if ((Q & 1) && a == QH) {
+      out[a] = odd ? O : E;
+    } else {
+      out[a] = E + O;
+      out[Q - 1 - a] = sg * (E - O);
+    }
+  }
+}
+
+// same, parity fixed at compile time (PAR = +1: B, -1: D)
+template <int N, int Q, int PAR>
+__device__ __forceinline__ void fg_fwd_c(const double* __restrict__ tab, const double (&in)[N], double (&out)[Q]) {
+  using F = Fold<N - 1, Q>;
+  constexpr int NE = F::NE, NH = F::NH, QE = F::QE, QH = F::QH;
+  double up[NE], um[F::NHX];
+#pragma unroll
+  for (int i = 0; i < NH; ++i) {
+    up[i] = in[i] + in[N - 1 - i];
+    um[i] = in[i] - in[N - 1 - i];
+  }
+  if (N & 1) up[NH] = in[NH];
+#pragma unroll
+  for (int a = 0; a < QE; ++a) {
+    const bool mid = (Q & 1) && a == QH;
+    double E = 0.0, O = 0.0;
+    if (!(mid && PAR < 0)) {
+#pragma unroll
+      for (int i = 0; i < NE; ++i) E = fma(tab[F::FE + a * NE + i], up[i], E);
+    }
+    if (!(mid && PAR > 0)) {
+#pragma unroll
+      for (int i = 0; i < NH; ++i) O = fma(tab[F::FO + a * NH + i], um[i], O);
+    }
+    out[a] = E + O;
+    if (!mid) out[Q - 1 - a] = PAR > 0 ? E - O : O - E;
+  }
+}
+
+// transposed folded contraction out[k] = sum_a T[a][k] in[a], parity at run time:
+// P1 = sum_{a<qe} TE[k][a] (in_a + in_{q-1-a}), P2 = sum_{a<qh} TO[k][a] (in_a - in_{q-1-a});
+// out[k] = P1 + P2, out[n-1-k] = sgn (P1 - P2); the middle node (n odd) takes P1 (B) or P2 (D)
+template <int N, int Q>
+__device__ __forceinline__ void fg_bwd(const double* __restrict__ tab, bool odd, const double (&in)[Q],
+                                       double (&out)[N]) {
+  using F = Fold<N - 1, Q>;
+  constexpr int NE = F::NE, NH = F::NH, QE = F::QE, QH = F::QH;
+  double vp[QE], vm[F::QHX];
+#pragma unroll
+  for (int a = 0; a < QH; ++a) {
+    vp[a] = in[a] + in[Q - 1 - a];
+    vm[a] = in[a] - in[Q - 1 - a];
+  }
+  if (Q & 1) vp[QH] = in[QH];
+  const double sg = odd ? -1.0 : 1.0;
+#pragma unroll
+  for (int k = 0; k < NE; ++k) {
+    double P1 = 0.0, P2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < QE; ++a) P1 = fma(tab[F::BE + k * QE + a], vp[a], P1);
+#pragma unroll
+    for (int a = 0; a < QH; ++a) P2 = fma(tab[F::BO + k * QH + a], vm[a], P2);
+    if ((N & 1) && k == NH) {
+      out[k] = odd ? P2 : P1;
+    } else {
+      out[k] = P1 + P2;
+      out[N - 1 - k] = sg * (P1 - P2);
+    }
+  }
+}
+
+// same, parity fixed at compile time
+template <int N, int Q, int PAR>
+__device__ __forceinline__ void fg_bwd_c(const double* __restrict__ tab, const double (&in)[Q], double (&out)[N]) {
+  using F = Fold<N - 1, Q>;
+  constexpr int NE = F::NE, NH = F::NH, QE = F::QE, QH = F::QH;
+  double vp[QE], vm[F::QHX];
+#pragma unroll
+  for (int a = 0; a < QH; ++a) {
+    vp[a] = in[a] + in[Q - 1 - a];
+    vm[a] = in[a] - in[Q - 1 - a];
+  }
+  if (Q & 1) vp[QH] = in[QH];
+#pragma unroll
+  for (int k = 0; k < NE; ++k) {
+    const bool kmid = (N & 1) && k == NH;
+    double P1 = 0.0, P2 = 0.0;
+    if (!(kmid && PAR < 0)) {
+#pragma unroll
+      for (int a = 0; a < QE; ++a) P1 = fma(tab[F::BE + k * QE + a], vp[a], P1);
+    }
+    if (!(kmid && PAR > 0)) {
+#pragma unroll
+      for (int a = 0; a < QH; ++a) P2 = fma(tab[F::BO + k * QH + a], vm[a], P2);
+    }
+    out[k] = P1 + P2;
+    if (!kmid) out[N - 1 - k] = PAR > 0 ? P1 - P2 : P2 - P1;
+  }
+}
+
+// out[k] = sum_a B[a][k] u[a] + D[a][k] w[a]   (B^T u + D^T w, both folded)
+template <int N, int Q>
+__device__ __forceinline__ void fg_bwd2(const double* __restrict__ tB, const double* __restrict__ tD,
+                                        const double (&u)[Q], const double (&w)[Q], double (&out)[N]) {
+  using F = Fold<N - 1, Q>;
+  constexpr int NE = F::NE, NH = F::NH, QE = F::QE, QH = F::QH;
+  double up[QE], um[F::QHX], wp[QE], wm[F::QHX];
+#pragma unroll
+  for (int a = 0; a < QH; ++a) {
+    up[a] = u[a] + u[Q - 1 - a];
+    um[a] = u[a] - u[Q - 1 - a];
+    wp[a] = w[a] + w[Q - 1 - a];
+    wm[a] = w[a] - w[Q - 1 - a];
+  }
+  if (Q & 1) {
+    up[QH] = u[QH];
+    wp[QH] = w[QH];
+  }
+#pragma unroll
+  for (int k = 0; k < NE; ++k) {
+    const bool kmid = (N & 1) && k == NH;
+    double X = 0.0, Y = 0.0;
+#pragma unroll
+    for (int a = 0; a < QE; ++a) X = fma(tB[F::BE + k * QE + a], up[a], X);
+#pragma unroll
+    for (int a = 0; a < QH; ++a) X = fma(tD[F::BO + k * QH + a], wm[a], X);
+    if (!kmid) {
+#pragma unroll
+      for (int a = 0; a < QE; ++a) Y = fma(tD[F::BE + k * QE + a], wp[a], Y);
+#pragma unroll
+      for (int a = 0; a < QH; ++a) Y = fma(tB[F::BO + k * QH + a], um[a], Y);
+      out[k] = X + Y;
+      out[N - 1 - k] = X - Y;
+    } else {
+      out[k] = X;
+    }
+  }
+}
+
+template <int P, int Q>
+__global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
+    apply_fg_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
+                    const double* __restrict__ rr, Slab s, int64_t e_begin, int64_t e_end) {
+  using C = CfgFG<P, Q>;
+  using F = Fold<P, Q>;
+  constexpr int N = C::N, NT = C::NT, QQ = Q * Q;
+  constexpr int CUN = ELAS_FG_CU1 ? 1 : 3;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* smem = reinterpret_cast<double*>(smem_raw);
+  const double* tB = ELAS_FG_CTAB ? c_fold<P, Q, double> : smem;
+  const double* tD = ELAS_FG_CTAB ? c_fold<P, Q, double> + F::TS : smem + F::TS;
+  double* sZ = smem + C::TAB;
+  double* sY = sZ + C::ZE;
+  const int tid = threadIdx.x;
+  const int64_t e = e_begin + blockIdx.x;
+  int ex, ey, ez;
+  {
+    const uint32_t l32 = (uint32_t)e, nx = (uint32_t)s.nx, ny = (uint32_t)s.ny;
+    const uint32_t exy = l32 / nx;
+    ex = (int)(l32 - exy * nx);
+    ez = (int)(exy / ny);
+    ey = (int)(exy - (uint32_t)ez * ny);
+  }
+  const int64_t plane = (int64_t)s.Nx * s.Ny;
+  const bool bc = s.faces != 0;
+  const double* qe = qd + e * (int64_t)C::QDE;
+#if ELAS_FG_PREF_OWN
+  if (tid == 0) {   // this element's quadrature data towards L2 (used after stages Z, Y, X)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qe), "r"((uint32_t)(C::QDE * sizeof(double)))
+                 : "memory");
+  }
+#endif
+
+  // ---- gather: item (c, j, i) = one z-column of component c (A1: u_e = G x) ----
+  const int gc = tid / (N * N), gj = (tid / N) % N, gi = tid % N;
+  const bool zcol = tid < 3 * N * N;
+  double u[N];
+  const int I = ex * P + gi, J = ey * P + gj;
+  const int64_t cbase = (int64_t)gc * s.nodes + I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
+  if (zcol) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      ELAS_DCHECK(cbase + k * plane < 3 * s.nodes && cbase >= 0);
+      u[k] = __ldg(x + cbase + k * plane);
+    }
+    if (bc) {
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+        if (is_constrained(I, J, ez * P + k, s)) u[k] = 0.0;
+    }
+  }
+  if (!ELAS_FG_CTAB)
+    for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = c_fold<P, Q, double>[t];
+  const double r = __ldg(rr + e);
+  __syncthreads();
+
+  // ---- Z: Zb = Bz u, Zd = Dz u (A2, first 1D contraction) ----
+  if (zcol) {
+    double zb[Q], zd[Q];
+    fg_fwd_c<N, Q, 1>(tB, u, zb);
+    fg_fwd_c<N, Q, -1>(tD, u, zd);
+    double* dst = sZ + gc * C::ZC + gj * N + gi;
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+      dst[a * C::SA] = zb[a];
+      dst[C::ZV + a * C::SA] = zd[a];
+    }
+  }
+  __syncthreads();
+
+  // ---- Y: item (c, a3, i): Y0 = By Zb, Y1 = Dy Zb, Y2 = By Zd ----
+  for (int t = tid; t < 3 * Q * N; t += NT) {
+    const int i = t % N, a3 = (t / N) % Q, c = t / (N * Q);
+    const double* src = sZ + c * C::ZC + a3 * C::SA + i;
+    double* dst = sY + c * C::YC + a3 * C::LN + i;
+    double zb[N], zd[N], o[Q];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      zb[j] = src[j * N];
+      zd[j] = src[C::ZV + j * N];
+    }
+    fg_fwd_c<N, Q, 1>(tB, zb, o);
+#pragma unroll
+    for (int a = 0; a < Q; ++a) dst[a * C::S2] = o[a];
+    fg_fwd_c<N, Q, -1>(tD, zb, o);
+#pragma unroll
+    for (int a = 0; a < Q; ++a) dst[C::YV + a * C::S2] = o[a];
+    fg_fwd_c<N, Q, 1>(tB, zd, o);
+#pragma unroll
+    for (int a = 0; a < Q; ++a) dst[2 * C::YV + a * C::S2] = o[a];
+  }
+  // the pointwise stage's quadrature data: the thread's first point in flight during stage X
+  constexpr int KP = (Q * QQ + NT - 1) / NT;   // points per thread
+  double Ak[KP][9];
+  if (tid < Q * QQ) {
+#pragma unroll
+    for (int f = 0; f < 9; ++f) Ak[0][f] = qe[(tid / QQ) * 9 * QQ + f * QQ + tid % QQ];
+  }
+  __syncthreads();
+
+  // gradient / flux slot (c, v) of line L at x-point a: the run itself for a < n, else overflow
+  auto gslot = [&](int c, int v, int L, int a) -> double* {
+    return a < N ? sY + c * C::YC + v * C::YV + L * C::LN + a
+                 : sZ + ((c * 3 + v) * QQ + L) * C::OVN + (a - N);
+  };
+  // stage X / Xt item for direction v with the parity fixed at compile time (the branch on v is
+  // warp-uniform where q^2 is a multiple of 32), so the coefficients stay constant-bank operands
+  auto xfwd = [&](auto par, int v, int L) {
+    constexpr int PAR = decltype(par)::value;
+    const double* tab = PAR < 0 ? tD : tB;
+#pragma unroll CUN
+    for (int c = 0; c < 3; ++c) {
+      double in[N], o[Q];
+      const double* src = sY + c * C::YC + v * C::YV + L * C::LN;
+#pragma unroll
+      for (int i = 0; i < N; ++i) in[i] = src[i];
+      fg_fwd_c<N, Q, PAR>(tab, in, o);
+#pragma unroll
+      for (int a = 0; a < Q; ++a) *gslot(c, v, L, a) = o[a];
+    }
+  };
+  auto xbwd = [&](auto par, int d, int L) {
+    constexpr int PAR = decltype(par)::value;
+    const double* tab = PAR < 0 ? tD : tB;
+#pragma unroll CUN
+    for (int c = 0; c < 3; ++c) {
+      double in[Q], o[N];
+#pragma unroll
+      for (int a = 0; a < Q; ++a) in[a] = *gslot(c, d, L, a);
+      fg_bwd_c<N, Q, PAR>(tab, in, o);
+      double* dst = sY + c * C::YC + d * C::YV + L * C::LN;
+#pragma unroll
+      for (int i = 0; i < N; ++i) dst[i] = o[i];
+    }
+  };
+
+  // ---- X: item (v, line): g[c][v] at the q points of the line, in place ----
+  for (int t = tid; t < 3 * QQ; t += NT) {
+    const int L = t % QQ, v = t / QQ;
+    if (v == 0) xfwd(std::integral_constant<int, -1>{}, 0, L);   // x-derivative: D table
+    else xfwd(std::integral_constant<int, 1>{}, v, L);
+  }
+  // the remaining points' quadrature data, all in flight together
+#pragma unroll
+  for (int k = 1; k < KP; ++k) {
+    const int t = tid + k * NT;
+    if (t < Q * QQ) {
+#pragma unroll
+      for (int f = 0; f < 9; ++f) Ak[k][f] = qe[(t / QQ) * 9 * QQ + f * QQ + t % QQ];
+    }
+  }
+  __syncthreads();
+
+  // ---- pointwise: item (a1, line): F = sigma~ A~^T at one point (A3, Eq. 3) ----
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    const int t = tid + k * NT;
+    if (t < Q * QQ) {
+      const int L = t % QQ, a1 = t / QQ;
+      double G[3][3];
+      double* gp[3][3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          gp[c][d] = gslot(c, d, L, a1);
+          G[c][d] = *gp[c][d];
+        }
+      pointwise_t<double>(G, Ak[k], r);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) *gp[c][d] = G[c][d];
+    }
+  }
+  __syncthreads();
+
+  // ---- Xt: item (d, line): run (c, d) <- (D or B)_x^T F[c][d] ----
+  for (int t = tid; t < 3 * QQ; t += NT) {
+    const int L = t % QQ, d = t / QQ;
+    if (d == 0) xbwd(std::integral_constant<int, -1>{}, 0, L);
+    else xbwd(std::integral_constant<int, 1>{}, d, L);
+  }
+  __syncthreads();
+
+  // ---- Yt: item (c, a3, i): Wb = By^T V0 + Dy^T V1, Wd = By^T V2 ----
+  for (int t = tid; t < 3 * Q * N; t += NT) {
+    const int i = t % N, a3 = (t / N) % Q, c = t / (N * Q);
+    const double* src = sY + c * C::YC + a3 * C::LN + i;
+    double* dst = sZ + c * C::ZC + a3 * C::SA + i;
+    double v0[Q], v1[Q], o[N];
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+      v0[a] = src[a * C::S2];
+      v1[a] = src[C::YV + a * C::S2];
+    }
+    fg_bwd2<N, Q>(tB, tD, v0, v1, o);
+#pragma unroll
+    for (int j = 0; j < N; ++j) dst[j * N] = o[j];
+#pragma unroll
+    for (int a = 0; a < Q; ++a) v0[a] = src[2 * C::YV + a * C::S2];
+    fg_bwd_c<N, Q, 1>(tB, v0, o);
+#pragma unroll
+    for (int j = 0; j < N; ++j) dst[C::ZV + j * N] = o[j];
+  }
+  __syncthreads();
+
+  // ---- Zt + scatter: item (c, j, i): y_col += Bz^T Wb + Dz^T Wd (A4, A5) ----
+  if (zcol) {
+    const double* src = sZ + gc * C::ZC + gj * N + gi;
+    double wb[Q], wd[Q], o[N];
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+      wb[a] = src[a * C::SA];
+      wd[a] = src[C::ZV + a * C::SA];
+    }
+    fg_bwd2<N, Q>(tB, tD, wb, wd, o);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      if (!(bc && is_constrained(I, J, ez * P + k, s))) {
+        ELAS_DCHECK(cbase + k * plane < 3 * s.nodes && cbase >= 0);
+        atomicAdd(y + cbase + k * plane, o[k]);
+      }
+    }
+  }
+}
+
+template <int P, int Q>
+cudaError_t launch_apply_fg(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
+                            int64_t e_begin, int64_t e_end, cudaStream_t st) {
+  using C = CfgFG<P, Q>;
+  static KernelPrep prep;
+  int pref = 0;
+  cudaError_t err = prep.prep(apply_fg_kernel<P, Q>, C::NT, C::smem, &pref);
+  if (err != cudaSuccess) return err;
+  const int64_t ne = e_end - e_begin;
+  if (ne <= 0) return cudaSuccess;
+  apply_fg_kernel<P, Q><<<(unsigned)ne, C::NT, C::smem, st>>>(x, y, static_cast<const double*>(qd), rr, s, e_begin,
+                                                               e_end);
+  return cudaGetLastError();
+}
+
+template <int P, int Q>
+void info_fg_pq(ApplyLaunch* info) {
+  using C = CfgFG<P, Q>;
+  info->threads = C::NT;
+  info->elems_per_cta = 1;
+  info->smem_bytes = C::smem;
+}
+
+}  // namespace elas
