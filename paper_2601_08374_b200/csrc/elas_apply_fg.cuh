@@ -30,8 +30,16 @@ namespace elas {
 #ifndef ELAS_FG_CTAB
 #define ELAS_FG_CTAB 1   // 1: coefficients read from the constant bank (no shared copy)
 #endif
+// L2 prefetch at CTA start for the element the next wave of CTAs on this SM takes (e + resident
+// CTAs): bit 0 its x columns (prefetch.global.L2, one per gathered word), bit 1 its qdata (one
+// cp.async.bulk.prefetch.L2).  ELAS_FG_PREF_OWN: the CTA's own qdata instead.  Measured (config 4
+// p6 / p7 / p8, config 5; GDoF/s): own qdata 39.35 / 34.36 / 32.39, 37.57; next-wave qdata 39.55 /
+// 35.02 / 33.21, 37.61; next-wave x 39.26 / 35.51 / 33.24, 36.60; both 38.97 / 35.48 / 32.90, 36.14.
+#ifndef ELAS_FG_PF
+#define ELAS_FG_PF 2
+#endif
 #ifndef ELAS_FG_PREF_OWN
-#define ELAS_FG_PREF_OWN 1   // L2 prefetch of the CTA's own qdata at start
+#define ELAS_FG_PREF_OWN 0
 #endif
 
 template <int P, int Q>
@@ -224,7 +232,7 @@ __device__ __forceinline__ void fg_bwd2(const double* __restrict__ tB, const dou
 template <int P, int Q>
 __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
     apply_fg_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
-                    const double* __restrict__ rr, Slab s, int64_t e_begin, int64_t e_end) {
+                    const double* __restrict__ rr, Slab s, int64_t e_begin, int64_t e_end, int pf) {
   using C = CfgFG<P, Q>;
   using F = Fold<P, Q>;
   constexpr int N = C::N, NT = C::NT, QQ = Q * Q;
@@ -276,6 +284,27 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   if (!ELAS_FG_CTAB)
     for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = c_fold<P, Q, double>[t];
   const double r = __ldg(rr + e);
+  if constexpr ((ELAS_FG_PF & 3) != 0) {   // the element the next wave of CTAs on this SM will take
+    const int64_t e2 = e + pf;
+    if (pf > 0 && e2 < e_end) {
+      if constexpr ((ELAS_FG_PF & 1) != 0) {
+        if (zcol) {
+          const uint32_t l2 = (uint32_t)e2, nx = (uint32_t)s.nx, ny = (uint32_t)s.ny;
+          const uint32_t exy2 = l2 / nx, ex2 = l2 - exy2 * nx, ez2 = exy2 / ny, ey2 = exy2 - ez2 * ny;
+          const double* xb2 = x + (int64_t)gc * s.nodes + (ex2 * P + gi) + (int64_t)s.Nx * (ey2 * P + gj) +
+                              plane * ((int64_t)ez2 * P);
+#pragma unroll
+          for (int k = 0; k < N; ++k) asm volatile("prefetch.global.L2 [%0];" ::"l"(xb2 + k * plane));
+        }
+      }
+      if constexpr ((ELAS_FG_PF & 2) != 0) {
+        if (tid == 32)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qd + e2 * (int64_t)C::QDE),
+                       "r"((uint32_t)(C::QDE * sizeof(double)))
+                       : "memory");
+      }
+    }
+  }
   __syncthreads();
 
   // ---- Z: Zb = Bz u, Zd = Dz u (A2, first 1D contraction) ----
@@ -460,7 +489,7 @@ cudaError_t launch_apply_fg(const Slab& s, const double* x, double* y, const voi
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
   apply_fg_kernel<P, Q><<<(unsigned)ne, C::NT, C::smem, st>>>(x, y, static_cast<const double*>(qd), rr, s, e_begin,
-                                                               e_end);
+                                                               e_end, pref);
   return cudaGetLastError();
 }
 
