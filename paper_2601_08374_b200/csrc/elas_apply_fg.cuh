@@ -42,10 +42,14 @@ namespace elas {
 #define ELAS_FG_PREF_OWN 0
 #endif
 
+#ifndef ELAS_FG_NT_P8
+#define ELAS_FG_NT_P8 0
+#endif
 template <int P, int Q>
 struct CfgFG {
   static constexpr int N = P + 1;
-  static constexpr int NT = ((3 * Q * Q + 31) / 32) * 32;   // one X item per thread
+  static constexpr int NT0 = ((3 * Q * Q + 31) / 32) * 32;   // one X item per thread
+  static constexpr int NT = (P == 8 && ELAS_FG_NT_P8 > 0) ? ELAS_FG_NT_P8 : NT0;
   static constexpr int LN = (N & 1) ? N : N + 1;             // odd line stride: X/pointwise conflict-free
   static constexpr int S2 = Q * LN;                          // => line (a2, a3) starts at (a2 q + a3) LN
   static constexpr int YV = Q * S2, YC = 3 * YV, YE = 3 * YC;
@@ -244,17 +248,47 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   double* sZ = smem + C::TAB;
   double* sY = sZ + C::ZE;
   const int tid = threadIdx.x;
-  const int64_t e = e_begin + blockIdx.x;
-  int ex, ey, ez;
-  {
-    const uint32_t l32 = (uint32_t)e, nx = (uint32_t)s.nx, ny = (uint32_t)s.ny;
+  const int64_t plane = (int64_t)s.Nx * s.Ny;
+  const bool bc = s.faces != 0;
+  // item (c, j, i) of the gather / Z / Zt stages: one z-column of component c
+  const int gc = tid / (N * N), gj = (tid / N) % N, gi = tid % N;
+  const bool zcol = tid < 3 * N * N;
+  auto coords = [&](int64_t el, int& ex, int& ey, int& ez) {
+    const uint32_t l32 = (uint32_t)el, nx = (uint32_t)s.nx, ny = (uint32_t)s.ny;
     const uint32_t exy = l32 / nx;
     ex = (int)(l32 - exy * nx);
     ez = (int)(exy / ny);
     ey = (int)(exy - (uint32_t)ez * ny);
-  }
-  const int64_t plane = (int64_t)s.Nx * s.Ny;
-  const bool bc = s.faces != 0;
+  };
+  // A1: u_e = G x, constrained entries zeroed (Z x)
+  double u[N];
+  auto gather = [&](int64_t el) {
+    if (!zcol) return;
+    int ex, ey, ez;
+    coords(el, ex, ey, ez);
+    const int I = ex * P + gi, J = ey * P + gj;
+    const int64_t cb = (int64_t)gc * s.nodes + I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      ELAS_DCHECK(cb + k * plane < 3 * s.nodes && cb >= 0);
+      u[k] = __ldg(x + cb + k * plane);
+    }
+    if (bc) {
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+        if (is_constrained(I, J, ez * P + k, s)) u[k] = 0.0;
+    }
+  };
+  const int64_t e0 = e_begin + blockIdx.x;
+  if (e0 < e_end) gather(e0);
+  if (!ELAS_FG_CTAB)
+    for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = c_fold<P, Q, double>[t];
+
+  auto body = [&](const int64_t e) {
+  int ex, ey, ez;
+  coords(e, ex, ey, ez);
+  const int I = ex * P + gi, J = ey * P + gj;
+  const int64_t cbase = (int64_t)gc * s.nodes + I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
   const double* qe = qd + e * (int64_t)C::QDE;
 #if ELAS_FG_PREF_OWN
   if (tid == 0) {   // this element's quadrature data towards L2 (used after stages Z, Y, X)
@@ -262,35 +296,15 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
                  : "memory");
   }
 #endif
-
-  // ---- gather: item (c, j, i) = one z-column of component c (A1: u_e = G x) ----
-  const int gc = tid / (N * N), gj = (tid / N) % N, gi = tid % N;
-  const bool zcol = tid < 3 * N * N;
-  double u[N];
-  const int I = ex * P + gi, J = ey * P + gj;
-  const int64_t cbase = (int64_t)gc * s.nodes + I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
-  if (zcol) {
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      ELAS_DCHECK(cbase + k * plane < 3 * s.nodes && cbase >= 0);
-      u[k] = __ldg(x + cbase + k * plane);
-    }
-    if (bc) {
-#pragma unroll
-      for (int k = 0; k < N; ++k)
-        if (is_constrained(I, J, ez * P + k, s)) u[k] = 0.0;
-    }
-  }
-  if (!ELAS_FG_CTAB)
-    for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = c_fold<P, Q, double>[t];
   const double r = __ldg(rr + e);
   if constexpr ((ELAS_FG_PF & 3) != 0) {   // the element the next wave of CTAs on this SM will take
-    const int64_t e2 = e + pf;
-    if (pf > 0 && e2 < e_end) {
+    const int64_t pfd = pf;
+    const int64_t e2 = e + pfd;
+    if (pfd > 0 && e2 < e_end) {
       if constexpr ((ELAS_FG_PF & 1) != 0) {
         if (zcol) {
-          const uint32_t l2 = (uint32_t)e2, nx = (uint32_t)s.nx, ny = (uint32_t)s.ny;
-          const uint32_t exy2 = l2 / nx, ex2 = l2 - exy2 * nx, ez2 = exy2 / ny, ey2 = exy2 - ez2 * ny;
+          int ex2, ey2, ez2;
+          coords(e2, ex2, ey2, ez2);
           const double* xb2 = x + (int64_t)gc * s.nodes + (ex2 * P + gi) + (int64_t)s.Nx * (ey2 * P + gj) +
                               plane * ((int64_t)ez2 * P);
 #pragma unroll
@@ -305,7 +319,7 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
       }
     }
   }
-  __syncthreads();
+  __syncthreads();   // u gathered
 
   // ---- Z: Zb = Bz u, Zd = Dz u (A2, first 1D contraction) ----
   if (zcol) {
@@ -476,6 +490,8 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
       }
     }
   }
+  };   // body (persistent CTAs walking several elements spilled 300-600 bytes: rejected)
+  if (e0 < e_end) body(e0);
 }
 
 template <int P, int Q>

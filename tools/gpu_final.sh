@@ -11,6 +11,6 @@ ARGS="--steps 3 --warmup 3 --no-sweep --no-cpu-baseline --no-solver --e2e-steps 
 timeout 900 python bench.py $ARGS > gpurun_out/ncu_plain.json 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg5.csv \
     python bench.py $ARGS > gpurun_out/ncu_launch.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:apply_eo -s 3 -c 1 -o gpurun_out/ncu_cfg5_eo -f \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:apply_ -s 3 -c 1 -o gpurun_out/ncu_cfg5_eo -f \
     python bench.py $ARGS > gpurun_out/ncu_full.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_full.log
 tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; head -c 400 gpurun_out/bench.json; tail -1 gpurun_out/ncu_full.log
