@@ -100,7 +100,10 @@ elas_op* elas_create_aniso(const elas_mesh* mesh, int p, int q, const double* C2
  *                       (p = 6, q = 8 only);
  *   ELAS_VARIANT_THREAD one thread per element, sum factorisation in registers (p = 1 only);
  *   ELAS_VARIANT_FOLDED the SIMT kernel with even-odd folded 1D contractions (every p, q;
- *                       half the sum-factorisation FMAs; same qdata layout as SIMT);
+ *                       half the sum-factorisation FMAs; same qdata layout as SIMT).  For
+ *                       FP64 at p = 6..8 (non-deterministic mode, stored geometry, isotropic)
+ *                       it runs as the fine-grained kernel: one element per CTA of 3 q^2
+ *                       threads, one-component / one-point work items;
  *   ELAS_VARIANT_FOLDED_F32  MIXED PRECISION (PAPER.md:600 future work): the folded kernel
  *                       with FP32 quadrature data (9 floats per point), FP32 tables and FP32
  *                       arithmetic; x, y stay FP64 (converted on gather, FP64 atomics on

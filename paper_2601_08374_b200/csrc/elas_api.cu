@@ -295,8 +295,10 @@ int build(elas_op* op, const elas_mesh* m, const double* lambda, const double* m
   return rc;
 }
 
-int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1, cudaStream_t st) {
+int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1, cudaStream_t st, bool acc = false) {
   if (e1 <= e0) return ELAS_OK;
+  Slab sl = op->slab;   // sl.accumulate: the fine-grained kernel's interior nodes take plain stores only when 0
+  sl.accumulate = acc ? 1u : 0u;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   if (op->prof) {
     while (op->prof_ev.size() < op->prof_used + 2) {
@@ -337,7 +339,7 @@ int range_apply(elas_op* op, const double* x, double* y, int64_t e0, int64_t e1,
                   : op->variant == ELAS_VARIANT_THREAD
                       ? elas::apply_p1t_launch(op->q, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st)
                   : op->variant == ELAS_VARIANT_FOLDED
-                      ? elas::apply_eo_launch(op->p, op->q, 0, op->slab, x, y, op->qd, op->rr, op->tab, e0, e1, st,
+                      ? elas::apply_eo_launch(op->p, op->q, 0, sl, x, y, op->qd, op->rr, op->tab, e0, e1, st,
                                               nullptr, 0, op->cc)
                   : op->variant == ELAS_VARIANT_FOLDED_F32
                       ? elas::apply_eo_launch(op->p, op->q, 1, op->slab, x, y, op->qd, op->rr, op->tabf, e0, e1, st)
@@ -785,7 +787,7 @@ int elas_apply_add(elas_op* op, const double* x, double* y) {
   }
   const Slab& s = op->slab;
   CUDA_OR(elas::launch_face_add(s, x, y, op->stream), "face add launch");
-  return range_apply(op, x, y, 0, (int64_t)s.nx * s.ny * s.nz, op->stream);
+  return range_apply(op, x, y, 0, (int64_t)s.nx * s.ny * s.nz, op->stream, true);
 }
 
 int elas_interface_add(elas_op* op, double* y, const double* lo_halo, const double* hi_halo) {

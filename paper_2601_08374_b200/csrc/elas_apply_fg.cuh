@@ -42,13 +42,23 @@ namespace elas {
 #define ELAS_FG_PREF_OWN 0
 #endif
 
+#ifndef ELAS_FG_ISTORE
+#define ELAS_FG_ISTORE 0   // element-interior nodes of y written with plain stores (one contribution)
+#endif
+#ifndef ELAS_FG_PADX_MASK
+#define ELAS_FG_PADX_MASK 0
+#endif
+template <int P> struct FgPadX { static constexpr bool value = ((ELAS_FG_PADX_MASK >> P) & 1) != 0; };
 #ifndef ELAS_FG_NT_P8
 #define ELAS_FG_NT_P8 0
 #endif
 template <int P, int Q>
 struct CfgFG {
   static constexpr int N = P + 1;
-  static constexpr int NT0 = ((3 * Q * Q + 31) / 32) * 32;   // one X item per thread
+  // X / Xt item space: 3 directions x QX lines, QX = q^2 or (PADX) q^2 rounded up to a warp so
+  // that no warp straddles two directions (the direction branch stays warp-uniform)
+  static constexpr int QX = FgPadX<P>::value ? ((Q * Q + 31) / 32) * 32 : Q * Q;
+  static constexpr int NT0 = ((3 * QX + 31) / 32) * 32;   // one X item per thread
   static constexpr int NT = (P == 8 && ELAS_FG_NT_P8 > 0) ? ELAS_FG_NT_P8 : NT0;
   static constexpr int LN = (N & 1) ? N : N + 1;             // odd line stride: X/pointwise conflict-free
   static constexpr int S2 = Q * LN;                          // => line (a2, a3) starts at (a2 q + a3) LN
@@ -402,8 +412,9 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   };
 
   // ---- X: item (v, line): g[c][v] at the q points of the line, in place ----
-  for (int t = tid; t < 3 * QQ; t += NT) {
-    const int L = t % QQ, v = t / QQ;
+  for (int t = tid; t < 3 * C::QX; t += NT) {
+    const int L = t % C::QX, v = t / C::QX;
+    if (C::QX != QQ && L >= QQ) continue;
     if (v == 0) xfwd(std::integral_constant<int, -1>{}, 0, L);   // x-derivative: D table
     else xfwd(std::integral_constant<int, 1>{}, v, L);
   }
@@ -443,8 +454,9 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   __syncthreads();
 
   // ---- Xt: item (d, line): run (c, d) <- (D or B)_x^T F[c][d] ----
-  for (int t = tid; t < 3 * QQ; t += NT) {
-    const int L = t % QQ, d = t / QQ;
+  for (int t = tid; t < 3 * C::QX; t += NT) {
+    const int L = t % C::QX, d = t / C::QX;
+    if (C::QX != QQ && L >= QQ) continue;
     if (d == 0) xbwd(std::integral_constant<int, -1>{}, 0, L);
     else xbwd(std::integral_constant<int, 1>{}, d, L);
   }
@@ -482,9 +494,14 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
       wd[a] = src[C::ZV + a * C::SA];
     }
     fg_bwd2<N, Q>(tB, tD, wb, wd, o);
+    // a node strictly inside the element gets this element's contribution only: with y zeroed
+    // beforehand (overwrite mode) a plain store replaces the atomic read-modify-write in L2
+    const bool icol = ELAS_FG_ISTORE && !s.accumulate && gi > 0 && gi < P && gj > 0 && gj < P;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      if (!(bc && is_constrained(I, J, ez * P + k, s))) {
+      if (k > 0 && k < P && icol) {
+        y[cbase + k * plane] = o[k];
+      } else if (!(bc && is_constrained(I, J, ez * P + k, s))) {
         ELAS_DCHECK(cbase + k * plane < 3 * s.nodes && cbase >= 0);
         atomicAdd(y + cbase + k * plane, o[k]);
       }

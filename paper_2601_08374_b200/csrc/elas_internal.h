@@ -57,6 +57,7 @@ struct Slab {
   int32_t Nx, Ny, Nz;        // nodes per axis (Nz = nz p + 1)
   int64_t nodes;             // Nx * Ny * Nz
   uint32_t faces;            // Dirichlet face bits, z faces already restricted to this slab
+  uint32_t accumulate;       // 1: y += A x (elas_apply_add): no plain stores of element-interior nodes
 };
 
 // Launch configuration the host needs for one (p, q) kernel instance.
