@@ -974,14 +974,24 @@ cudaError_t launch_apply_eo_pqc(const Slab& s, const double* x, double* y, const
 
 // fine-grained FP64 kernel (elas_apply_fg.cuh), per-degree mask (bit p).  Measured (config 4,
 // GDoF/s, x-line -> FG): p6 33.46 -> 39.36, p7 26.89 -> 34.31, p8 30.29 -> 32.41, config 5 33.55 ->
-// 37.51; p3 23.90 -> 16.86, p4 28.42 -> 25.63, p5 30.48 -> 27.27 stay on the x-line kernel.
+// 37.51, p5 30.48 -> 30.87 (warp-padded X items, 4 CTAs/SM); p3 23.90 -> 16.86, p4 28.42 -> 25.63
+// stay on the x-line kernel.
 #ifndef ELAS_FG_MASK
-#define ELAS_FG_MASK 0x1C0
+#define ELAS_FG_MASK 0x1E0
 #endif
 template <int P> struct FgOn { static constexpr bool value = ((ELAS_FG_MASK >> P) & 1) != 0; };
+#ifndef ELAS_FG_COLORED
+#define ELAS_FG_COLORED 1   // deterministic (colored) mode on the fine-grained kernel too (config 4 p6: 27.1 -> 36.1 GDoF/s)
+#endif
+template <int P> struct FgColored { static constexpr bool value = ELAS_FG_COLORED != 0; };
+#ifndef ELAS_FG_OTF
+#define ELAS_FG_OTF 0   // geometry on the fly on the fine-grained kernel too
+#endif
+template <int P> struct FgOtf { static constexpr bool value = ELAS_FG_OTF != 0; };
 template <int P, int Q>
 cudaError_t launch_apply_fg(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
-                            int64_t e_begin, int64_t e_end, cudaStream_t st);
+                            int64_t e_begin, int64_t e_end, cudaStream_t st, const ColorMap& cm, int otf,
+                            const double* tables);
 template <int P, int Q> void info_fg_pq(ApplyLaunch* info);
 
 template <int P, int Q, typename T>
@@ -989,7 +999,8 @@ cudaError_t launch_apply_eo_pq(const Slab& s, const double* x, double* y, const 
                                const void* tables, int64_t e_begin, int64_t e_end, cudaStream_t st,
                                const ColorMap& cm, int otf, const double* cc) {
   if constexpr (sizeof(T) == 8 && FgOn<P>::value) {
-    if (!cm.on && !otf && !cc) return launch_apply_fg<P, Q>(s, x, y, qd, rr, e_begin, e_end, st);
+    if (!cc && (!cm.on || FgColored<P>::value) && (!otf || FgOtf<P>::value))
+      return launch_apply_fg<P, Q>(s, x, y, qd, rr, e_begin, e_end, st, cm, otf, static_cast<const double*>(tables));
   }
   if constexpr (sizeof(T) == 8) {
     if (cc)

@@ -42,11 +42,8 @@ namespace elas {
 #define ELAS_FG_PREF_OWN 0
 #endif
 
-#ifndef ELAS_FG_ISTORE
-#define ELAS_FG_ISTORE 0   // element-interior nodes of y written with plain stores (one contribution)
-#endif
 #ifndef ELAS_FG_PADX_MASK
-#define ELAS_FG_PADX_MASK 0
+#define ELAS_FG_PADX_MASK 0x20   // p5: 49 lines -> 64 per direction (config 4: 28.2 -> 30.9 GDoF/s at 4 CTAs/SM)
 #endif
 template <int P> struct FgPadX { static constexpr bool value = ((ELAS_FG_PADX_MASK >> P) & 1) != 0; };
 #ifndef ELAS_FG_NT_P8
@@ -68,6 +65,9 @@ struct CfgFG {
   static constexpr int OVN = Q > N ? Q - N : 0;             // overflow slots per run (q > n)
   static constexpr int TAB = (2 * Fold<P, Q>::TS + 1) & ~1;
   static constexpr size_t smem = sizeof(double) * (size_t)(TAB + ZE + YE);
+  // geometry on the fly: Gauss points, sqrt weights and the element's trilinear-map words
+  static constexpr int OFFG = TAB + ZE + YE;
+  static constexpr size_t smem_otf = sizeof(double) * (size_t)(OFFG + 2 * Q + GEO_WORDS);
   static_assert(9 * Q * Q * OVN <= ZE, "gradient overflow must fit in the Z tile");
   static_assert(3 * N * N <= NT, "one z-column item per thread");
   static constexpr int QDE = qd_stride_words(Q, 8);
@@ -77,7 +77,7 @@ struct CfgFG {
 #endif
 template <int P> struct FgMinb {
   static constexpr int value = (P == 8 && ELAS_FG_MINB_P8 > 0) ? ELAS_FG_MINB_P8
-                               : ELAS_FG_MINB > 0 ? ELAS_FG_MINB : (P <= 4 ? 4 : P <= 6 ? 3 : 2);
+                               : ELAS_FG_MINB > 0 ? ELAS_FG_MINB : (P <= 5 ? 4 : P <= 6 ? 3 : 2);
 };
 #ifndef ELAS_FG_CU1
 #define ELAS_FG_CU1 0   // 1: component loops of stages X / Xt not unrolled (fewer live registers)
@@ -243,10 +243,43 @@ __device__ __forceinline__ void fg_bwd2(const double* __restrict__ tB, const dou
   }
 }
 
-template <int P, int Q>
+// A~ = sqrt(mu W) J^{-1} at point (a1, a2, a3) from the element's trilinear-map words (geometry on
+// the fly, QD_LAYOUT_OTF; same formulas as the x-line kernel's OTF path): along x, dx/dxi1 is
+// constant and dx/dxi2, dx/dxi3 are linear in xi1; A~ = sqrt(mu) sqrt(w1 w2 w3) adj(J) / sqrt(det J)
+__device__ __forceinline__ void fg_otf_A(const double* __restrict__ gs, int Q, int a1, int a2, int a3,
+                                         double (&A)[9]) {
+  const double* ge = gs + 2 * Q;
+  const double xi1 = gs[a1], xi2 = gs[a2], xi3 = gs[a3];
+  double J[3][3];
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    J[m][0] = fma(fma(ge[9 + m], xi3, ge[3 + m]), xi2, fma(ge[6 + m], xi3, ge[m]));
+    J[m][1] = fma(fma(ge[21 + m], xi3, ge[15 + m]), xi1, fma(ge[18 + m], xi3, ge[12 + m]));
+    J[m][2] = fma(fma(ge[33 + m], xi2, ge[27 + m]), xi1, fma(ge[30 + m], xi2, ge[24 + m]));
+  }
+  double adj[3][3];
+  adj[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+  adj[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+  adj[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+  adj[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+  adj[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+  adj[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+  adj[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  adj[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+  adj[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  const double det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
+  const double sc = ge[36] * gs[Q + a2] * gs[Q + a3] * gs[Q + a1] * rsqrt(det);
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int m = 0; m < 3; ++m) A[3 * d + m] = sc * adj[d][m];
+}
+
+template <int P, int Q, bool COLORED, bool OTF>
 __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
     apply_fg_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
-                    const double* __restrict__ rr, Slab s, int64_t e_begin, int64_t e_end, int pf) {
+                    const double* __restrict__ rr, Slab s, int64_t e_begin, int64_t e_end, int pf, ColorMap cm,
+                    const double* __restrict__ tables) {
   using C = CfgFG<P, Q>;
   using F = Fold<P, Q>;
   constexpr int N = C::N, NT = C::NT, QQ = Q * Q;
@@ -263,12 +296,10 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   // item (c, j, i) of the gather / Z / Zt stages: one z-column of component c
   const int gc = tid / (N * N), gj = (tid / N) % N, gi = tid % N;
   const bool zcol = tid < 3 * N * N;
-  auto coords = [&](int64_t el, int& ex, int& ey, int& ez) {
-    const uint32_t l32 = (uint32_t)el, nx = (uint32_t)s.nx, ny = (uint32_t)s.ny;
-    const uint32_t exy = l32 / nx;
-    ex = (int)(l32 - exy * nx);
-    ez = (int)(exy / ny);
-    ey = (int)(exy - (uint32_t)ez * ny);
+  // launch index -> element coordinates and element id (colored mode: the color's lattice,
+  // one contribution per node per launch; elas_apply_eo.cuh ColorMap)
+  auto coords = [&](int64_t el, int& ex, int& ey, int& ez) -> int64_t {
+    return elem_coords<COLORED>(cm, s, el, ex, ey, ez);
   };
   // A1: u_e = G x, constrained entries zeroed (Z x)
   double u[N];
@@ -296,18 +327,23 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
 
   auto body = [&](const int64_t e) {
   int ex, ey, ez;
-  coords(e, ex, ey, ez);
+  const int64_t eid = coords(e, ex, ey, ez);
   const int I = ex * P + gi, J = ey * P + gj;
   const int64_t cbase = (int64_t)gc * s.nodes + I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
-  const double* qe = qd + e * (int64_t)C::QDE;
+  const double* qe = qd + eid * (int64_t)C::QDE;
 #if ELAS_FG_PREF_OWN
   if (tid == 0) {   // this element's quadrature data towards L2 (used after stages Z, Y, X)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qe), "r"((uint32_t)(C::QDE * sizeof(double)))
                  : "memory");
   }
 #endif
-  const double r = __ldg(rr + e);
-  if constexpr ((ELAS_FG_PF & 3) != 0) {   // the element the next wave of CTAs on this SM will take
+  const double r = __ldg(rr + eid);
+  double* gsm = smem + C::OFFG;
+  if constexpr (OTF) {   // read only in the pointwise stage, several barriers later
+    for (int t = tid; t < 2 * Q; t += NT) gsm[t] = tables[2 * Q * N + 2 * F::TS + t];
+    for (int t = tid; t < GEO_WORDS; t += NT) gsm[2 * Q + t] = qd[eid * GEO_WORDS + t];
+  }
+  if constexpr ((ELAS_FG_PF & 3) != 0 && !OTF) {   // the element the next wave of CTAs on this SM will take
     const int64_t pfd = pf;
     const int64_t e2 = e + pfd;
     if (pfd > 0 && e2 < e_end) {
@@ -322,10 +358,13 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
         }
       }
       if constexpr ((ELAS_FG_PF & 2) != 0) {
-        if (tid == 32)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qd + e2 * (int64_t)C::QDE),
+        if (tid == 32) {
+          int ex2, ey2, ez2;
+          const int64_t eid2 = coords(e2, ex2, ey2, ez2);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qd + eid2 * (int64_t)C::QDE),
                        "r"((uint32_t)(C::QDE * sizeof(double)))
                        : "memory");
+        }
       }
     }
   }
@@ -368,8 +407,8 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   }
   // the pointwise stage's quadrature data: the thread's first point in flight during stage X
   constexpr int KP = (Q * QQ + NT - 1) / NT;   // points per thread
-  double Ak[KP][9];
-  if (tid < Q * QQ) {
+  double Ak[OTF ? 1 : KP][9];
+  if (!OTF && tid < Q * QQ) {
 #pragma unroll
     for (int f = 0; f < 9; ++f) Ak[0][f] = qe[(tid / QQ) * 9 * QQ + f * QQ + tid % QQ];
   }
@@ -420,7 +459,7 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   }
   // the remaining points' quadrature data, all in flight together
 #pragma unroll
-  for (int k = 1; k < KP; ++k) {
+  for (int k = 1; k < (OTF ? 1 : KP); ++k) {
     const int t = tid + k * NT;
     if (t < Q * QQ) {
 #pragma unroll
@@ -444,7 +483,13 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
           gp[c][d] = gslot(c, d, L, a1);
           G[c][d] = *gp[c][d];
         }
-      pointwise_t<double>(G, Ak[k], r);
+      if constexpr (OTF) {
+        double A[9];
+        fg_otf_A(gsm, Q, a1, L / Q, L % Q, A);
+        pointwise_t<double>(G, A, r);
+      } else {
+        pointwise_t<double>(G, Ak[k], r);
+      }
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -494,14 +539,11 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
       wd[a] = src[C::ZV + a * C::SA];
     }
     fg_bwd2<N, Q>(tB, tD, wb, wd, o);
-    // a node strictly inside the element gets this element's contribution only: with y zeroed
-    // beforehand (overwrite mode) a plain store replaces the atomic read-modify-write in L2
-    const bool icol = ELAS_FG_ISTORE && !s.accumulate && gi > 0 && gi < P && gj > 0 && gj < P;
+    // (measured and rejected: plain stores for the element-interior nodes, which get one
+    // contribution each: config 4 p6 39.6 -> 37.6 GDoF/s, config 5 36.0 -> 34.3)
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      if (k > 0 && k < P && icol) {
-        y[cbase + k * plane] = o[k];
-      } else if (!(bc && is_constrained(I, J, ez * P + k, s))) {
+      if (!(bc && is_constrained(I, J, ez * P + k, s))) {
         ELAS_DCHECK(cbase + k * plane < 3 * s.nodes && cbase >= 0);
         atomicAdd(y + cbase + k * plane, o[k]);
       }
@@ -511,19 +553,32 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   if (e0 < e_end) body(e0);
 }
 
-template <int P, int Q>
-cudaError_t launch_apply_fg(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
-                            int64_t e_begin, int64_t e_end, cudaStream_t st) {
+template <int P, int Q, bool COLORED, bool OTF>
+cudaError_t launch_apply_fg_c(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
+                              int64_t e_begin, int64_t e_end, cudaStream_t st, const ColorMap& cm,
+                              const double* tables) {
   using C = CfgFG<P, Q>;
+  constexpr size_t SMEM = OTF ? C::smem_otf : C::smem;
   static KernelPrep prep;
   int pref = 0;
-  cudaError_t err = prep.prep(apply_fg_kernel<P, Q>, C::NT, C::smem, &pref);
+  cudaError_t err = prep.prep(apply_fg_kernel<P, Q, COLORED, OTF>, C::NT, SMEM, &pref);
   if (err != cudaSuccess) return err;
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
-  apply_fg_kernel<P, Q><<<(unsigned)ne, C::NT, C::smem, st>>>(x, y, static_cast<const double*>(qd), rr, s, e_begin,
-                                                               e_end, pref);
+  apply_fg_kernel<P, Q, COLORED, OTF><<<(unsigned)ne, C::NT, SMEM, st>>>(
+      x, y, static_cast<const double*>(qd), rr, s, e_begin, e_end, pref, cm, tables);
   return cudaGetLastError();
+}
+
+template <int P, int Q>
+cudaError_t launch_apply_fg(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
+                            int64_t e_begin, int64_t e_end, cudaStream_t st, const ColorMap& cm, int otf,
+                            const double* tables) {
+  if (otf)
+    return cm.on ? launch_apply_fg_c<P, Q, true, true>(s, x, y, qd, rr, e_begin, e_end, st, cm, tables)
+                 : launch_apply_fg_c<P, Q, false, true>(s, x, y, qd, rr, e_begin, e_end, st, cm, tables);
+  return cm.on ? launch_apply_fg_c<P, Q, true, false>(s, x, y, qd, rr, e_begin, e_end, st, cm, tables)
+               : launch_apply_fg_c<P, Q, false, false>(s, x, y, qd, rr, e_begin, e_end, st, cm, tables);
 }
 
 template <int P, int Q>
