@@ -985,7 +985,8 @@ template <int P> struct FgOn { static constexpr bool value = ((ELAS_FG_MASK >> P
 #endif
 template <int P> struct FgColored { static constexpr bool value = ELAS_FG_COLORED != 0; };
 #ifndef ELAS_FG_OTF
-#define ELAS_FG_OTF 0   // geometry on the fly on the fine-grained kernel too
+#define ELAS_FG_OTF 1   // geometry on the fly on the fine-grained kernel too (config 4 GDoF/s x-line -> FG:
+                        // p5 27.7 -> 28.1, p6 33.6 -> 34.8, p7 24.3 -> 32.2, p8 30.0 -> 33.1; config 5 33.7 -> 34.8)
 #endif
 template <int P> struct FgOtf { static constexpr bool value = ELAS_FG_OTF != 0; };
 template <int P, int Q>
