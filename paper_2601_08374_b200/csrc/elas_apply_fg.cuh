@@ -27,28 +27,17 @@ namespace elas {
 #ifndef ELAS_FG_MINB
 #define ELAS_FG_MINB 0   // 0: per-degree default below
 #endif
-#ifndef ELAS_FG_CTAB
-#define ELAS_FG_CTAB 1   // 1: coefficients read from the constant bank (no shared copy)
-#endif
-// L2 prefetch at CTA start for the element the next wave of CTAs on this SM takes (e + resident
-// CTAs): bit 0 its x columns (prefetch.global.L2, one per gathered word), bit 1 its qdata (one
-// cp.async.bulk.prefetch.L2).  ELAS_FG_PREF_OWN: the CTA's own qdata instead.  Measured (config 4
-// p6 / p7 / p8, config 5; GDoF/s): own qdata 39.35 / 34.36 / 32.39, 37.57; next-wave qdata 39.55 /
-// 35.02 / 33.21, 37.61; next-wave x 39.26 / 35.51 / 33.24, 36.60; both 38.97 / 35.48 / 32.90, 36.14.
-#ifndef ELAS_FG_PF
-#define ELAS_FG_PF 2
-#endif
-#ifndef ELAS_FG_PREF_OWN
-#define ELAS_FG_PREF_OWN 0
-#endif
-
+// Measured and rejected knobs (profiles/r02_ab_round2.md, "Session 3"; removed from the code):
+// coefficients from a shared-memory copy instead of the constant bank (p6 31.2 -> 28.6), component
+// loops of X/Xt rolled (39.4 -> 25.4), L2 prefetch of the CTA's own qdata instead of the next
+// wave's (p7 35.0 -> 34.4, p8 33.2 -> 32.4), L2 prefetch of the next wave's x columns (config 5
+// 37.6 -> 36.6), CTA sizes 256 at p6 (39.6 -> 38.4) and 288 at p7 (34.1 -> 34.0), p8 at 1 CTA/SM
+// (163 registers: 22.3 -> 20.5) and at 352 threads (120-byte spills), the gather with the
+// L2::256B hint (no change), interior plain stores (39.6 -> 37.6), persistent CTAs (spills).
 #ifndef ELAS_FG_PADX_MASK
 #define ELAS_FG_PADX_MASK 0x20   // p5: 49 lines -> 64 per direction (config 4: 28.2 -> 30.9 GDoF/s at 4 CTAs/SM)
 #endif
 template <int P> struct FgPadX { static constexpr bool value = ((ELAS_FG_PADX_MASK >> P) & 1) != 0; };
-#ifndef ELAS_FG_NT_P8
-#define ELAS_FG_NT_P8 0
-#endif
 template <int P, int Q>
 struct CfgFG {
   static constexpr int N = P + 1;
@@ -56,7 +45,7 @@ struct CfgFG {
   // that no warp straddles two directions (the direction branch stays warp-uniform)
   static constexpr int QX = FgPadX<P>::value ? ((Q * Q + 31) / 32) * 32 : Q * Q;
   static constexpr int NT0 = ((3 * QX + 31) / 32) * 32;   // one X item per thread
-  static constexpr int NT = (P == 8 && ELAS_FG_NT_P8 > 0) ? ELAS_FG_NT_P8 : NT0;
+  static constexpr int NT = NT0;
   static constexpr int LN = (N & 1) ? N : N + 1;             // odd line stride: X/pointwise conflict-free
   static constexpr int S2 = Q * LN;                          // => line (a2, a3) starts at (a2 q + a3) LN
   static constexpr int YV = Q * S2, YC = 3 * YV, YE = 3 * YC;
@@ -72,16 +61,9 @@ struct CfgFG {
   static_assert(3 * N * N <= NT, "one z-column item per thread");
   static constexpr int QDE = qd_stride_words(Q, 8);
 };
-#ifndef ELAS_FG_MINB_P8
-#define ELAS_FG_MINB_P8 0
-#endif
 template <int P> struct FgMinb {
-  static constexpr int value = (P == 8 && ELAS_FG_MINB_P8 > 0) ? ELAS_FG_MINB_P8
-                               : ELAS_FG_MINB > 0 ? ELAS_FG_MINB : (P <= 5 ? 4 : P <= 6 ? 3 : 2);
+  static constexpr int value = ELAS_FG_MINB > 0 ? ELAS_FG_MINB : (P <= 5 ? 4 : P <= 6 ? 3 : 2);
 };
-#ifndef ELAS_FG_CU1
-#define ELAS_FG_CU1 0   // 1: component loops of stages X / Xt not unrolled (fewer live registers)
-#endif
 
 // forward folded contraction, parity chosen at run time (odd: D table, antisymmetric):
 // out[a] = E + O, out[q-1-a] = sgn (E - O); the middle point (q odd) takes E (B) or O (D)
@@ -283,11 +265,12 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   using C = CfgFG<P, Q>;
   using F = Fold<P, Q>;
   constexpr int N = C::N, NT = C::NT, QQ = Q * Q;
-  constexpr int CUN = ELAS_FG_CU1 ? 1 : 3;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* smem = reinterpret_cast<double*>(smem_raw);
-  const double* tB = ELAS_FG_CTAB ? c_fold<P, Q, double> : smem;
-  const double* tD = ELAS_FG_CTAB ? c_fold<P, Q, double> + F::TS : smem + F::TS;
+  // folded B | D tables as constant-bank operands (LDCU into uniform registers): every index is
+  // a compile-time constant after unrolling
+  const double* tB = c_fold<P, Q, double>;
+  const double* tD = c_fold<P, Q, double> + F::TS;
   double* sZ = smem + C::TAB;
   double* sY = sZ + C::ZE;
   const int tid = threadIdx.x;
@@ -322,8 +305,6 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   };
   const int64_t e0 = e_begin + blockIdx.x;
   if (e0 < e_end) gather(e0);
-  if (!ELAS_FG_CTAB)
-    for (int t = tid; t < 2 * F::TS; t += NT) smem[t] = c_fold<P, Q, double>[t];
 
   auto body = [&](const int64_t e) {
   int ex, ey, ez;
@@ -331,41 +312,20 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   const int I = ex * P + gi, J = ey * P + gj;
   const int64_t cbase = (int64_t)gc * s.nodes + I + (int64_t)s.Nx * J + plane * ((int64_t)ez * P);
   const double* qe = qd + eid * (int64_t)C::QDE;
-#if ELAS_FG_PREF_OWN
-  if (tid == 0) {   // this element's quadrature data towards L2 (used after stages Z, Y, X)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qe), "r"((uint32_t)(C::QDE * sizeof(double)))
-                 : "memory");
-  }
-#endif
   const double r = __ldg(rr + eid);
   double* gsm = smem + C::OFFG;
   if constexpr (OTF) {   // read only in the pointwise stage, several barriers later
     for (int t = tid; t < 2 * Q; t += NT) gsm[t] = tables[2 * Q * N + 2 * F::TS + t];
     for (int t = tid; t < GEO_WORDS; t += NT) gsm[2 * Q + t] = qd[eid * GEO_WORDS + t];
   }
-  if constexpr ((ELAS_FG_PF & 3) != 0 && !OTF) {   // the element the next wave of CTAs on this SM will take
-    const int64_t pfd = pf;
-    const int64_t e2 = e + pfd;
-    if (pfd > 0 && e2 < e_end) {
-      if constexpr ((ELAS_FG_PF & 1) != 0) {
-        if (zcol) {
-          int ex2, ey2, ez2;
-          coords(e2, ex2, ey2, ez2);
-          const double* xb2 = x + (int64_t)gc * s.nodes + (ex2 * P + gi) + (int64_t)s.Nx * (ey2 * P + gj) +
-                              plane * ((int64_t)ez2 * P);
-#pragma unroll
-          for (int k = 0; k < N; ++k) asm volatile("prefetch.global.L2 [%0];" ::"l"(xb2 + k * plane));
-        }
-      }
-      if constexpr ((ELAS_FG_PF & 2) != 0) {
-        if (tid == 32) {
-          int ex2, ey2, ez2;
-          const int64_t eid2 = coords(e2, ex2, ey2, ez2);
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qd + eid2 * (int64_t)C::QDE),
-                       "r"((uint32_t)(C::QDE * sizeof(double)))
-                       : "memory");
-        }
-      }
+  if constexpr (!OTF) {   // the qdata of the element the next wave of CTAs on this SM takes (e + pf)
+    const int64_t e2 = e + pf;
+    if (pf > 0 && e2 < e_end && tid == 32) {
+      int ex2, ey2, ez2;
+      const int64_t eid2 = coords(e2, ex2, ey2, ez2);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qd + eid2 * (int64_t)C::QDE),
+                   "r"((uint32_t)(C::QDE * sizeof(double)))
+                   : "memory");
     }
   }
   __syncthreads();   // u gathered
@@ -424,7 +384,7 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   auto xfwd = [&](auto par, int v, int L) {
     constexpr int PAR = decltype(par)::value;
     const double* tab = PAR < 0 ? tD : tB;
-#pragma unroll CUN
+#pragma unroll
     for (int c = 0; c < 3; ++c) {
       double in[N], o[Q];
       const double* src = sY + c * C::YC + v * C::YV + L * C::LN;
@@ -438,7 +398,7 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   auto xbwd = [&](auto par, int d, int L) {
     constexpr int PAR = decltype(par)::value;
     const double* tab = PAR < 0 ? tD : tB;
-#pragma unroll CUN
+#pragma unroll
     for (int c = 0; c < 3; ++c) {
       double in[Q], o[N];
 #pragma unroll
