@@ -34,6 +34,9 @@ namespace elas {
 // 37.6 -> 36.6), CTA sizes 256 at p6 (39.6 -> 38.4) and 288 at p7 (34.1 -> 34.0), p8 at 1 CTA/SM
 // (163 registers: 22.3 -> 20.5) and at 352 threads (120-byte spills), the gather with the
 // L2::256B hint (no change), interior plain stores (39.6 -> 37.6), persistent CTAs (spills).
+#ifndef ELAS_FG_KPF
+#define ELAS_FG_KPF 8   // at most this many pointwise points' qdata in flight per thread
+#endif
 #ifndef ELAS_FG_PADX_MASK
 #define ELAS_FG_PADX_MASK 0x20   // p5: 49 lines -> 64 per direction (config 4: 28.2 -> 30.9 GDoF/s at 4 CTAs/SM)
 #endif
@@ -367,7 +370,9 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   }
   // the pointwise stage's quadrature data: the thread's first point in flight during stage X
   constexpr int KP = (Q * QQ + NT - 1) / NT;   // points per thread
-  double Ak[OTF ? 1 : KP][9];
+  // points whose qdata is in flight before the stage (the rest, p8's partial 4th round, in-loop)
+  constexpr int KPF = KP > ELAS_FG_KPF ? ELAS_FG_KPF : KP;
+  double Ak[OTF ? 1 : KPF][9];
   if (!OTF && tid < Q * QQ) {
 #pragma unroll
     for (int f = 0; f < 9; ++f) Ak[0][f] = qe[(tid / QQ) * 9 * QQ + f * QQ + tid % QQ];
@@ -419,7 +424,7 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   }
   // the remaining points' quadrature data, all in flight together
 #pragma unroll
-  for (int k = 1; k < (OTF ? 1 : KP); ++k) {
+  for (int k = 1; k < (OTF ? 1 : KPF); ++k) {
     const int t = tid + k * NT;
     if (t < Q * QQ) {
 #pragma unroll
@@ -447,8 +452,13 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
         double A[9];
         fg_otf_A(gsm, Q, a1, L / Q, L % Q, A);
         pointwise_t<double>(G, A, r);
+      } else if (k < KPF) {
+        pointwise_t<double>(G, Ak[k < KPF ? k : 0], r);
       } else {
-        pointwise_t<double>(G, Ak[k], r);
+        double A[9];
+#pragma unroll
+        for (int f = 0; f < 9; ++f) A[f] = qe[a1 * 9 * QQ + f * QQ + L];
+        pointwise_t<double>(G, A, r);
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c)

@@ -10,7 +10,8 @@ KEYS = {"kernel": "Kernel Name", "ms": "gpu__time_duration.sum", "regs": "launch
         "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
         "smem_bank_conflicts": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "inst_executed": "smsp__inst_executed.sum", "grid": "launch__grid_size",
-        "l2_hit_pct": "lts__t_sector_hit_rate.pct"}
+        "l2_hit_pct": "lts__t_sector_hit_rate.pct",
+        "l1_data_pipe_pct": "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"}
 out = {}
 for p in range(1, 9):
     raw = subprocess.run(["ncu", "-i", f"gpurun_out/ncu_allp_{p}.ncu-rep", "--page", "raw", "--csv"],
