@@ -34,9 +34,13 @@ namespace elas {
 // 37.6 -> 36.6), CTA sizes 256 at p6 (39.6 -> 38.4) and 288 at p7 (34.1 -> 34.0), p8 at 1 CTA/SM
 // (163 registers: 22.3 -> 20.5) and at 352 threads (120-byte spills), the gather with the
 // L2::256B hint (no change), interior plain stores (39.6 -> 37.6), persistent CTAs (spills).
+// at most this many pointwise points' qdata in flight per thread (the rest loaded in-loop);
+// measured (config 4 GDoF/s, all / 3 / 2): p6 39.57 / 39.56 / 38.29, p7 34.10 / 34.08 / 33.70,
+// p8 33.15 / 33.31 / 33.85 (p8's 4-point prefetch spilled 28 bytes)
 #ifndef ELAS_FG_KPF
-#define ELAS_FG_KPF 8   // at most this many pointwise points' qdata in flight per thread
+#define ELAS_FG_KPF 0
 #endif
+template <int P> struct FgKpf { static constexpr int value = ELAS_FG_KPF > 0 ? ELAS_FG_KPF : P == 8 ? 2 : 8; };
 #ifndef ELAS_FG_PADX_MASK
 #define ELAS_FG_PADX_MASK 0x20   // p5: 49 lines -> 64 per direction (config 4: 28.2 -> 30.9 GDoF/s at 4 CTAs/SM)
 #endif
@@ -371,7 +375,7 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   // the pointwise stage's quadrature data: the thread's first point in flight during stage X
   constexpr int KP = (Q * QQ + NT - 1) / NT;   // points per thread
   // points whose qdata is in flight before the stage (the rest, p8's partial 4th round, in-loop)
-  constexpr int KPF = KP > ELAS_FG_KPF ? ELAS_FG_KPF : KP;
+  constexpr int KPF = KP > FgKpf<P>::value ? FgKpf<P>::value : KP;
   double Ak[OTF ? 1 : KPF][9];
   if (!OTF && tid < Q * QQ) {
 #pragma unroll
