@@ -41,6 +41,13 @@ namespace elas {
 #define ELAS_FG_KPF 0
 #endif
 template <int P> struct FgKpf { static constexpr int value = ELAS_FG_KPF > 0 ? ELAS_FG_KPF : P == 8 ? 2 : 8; };
+// L2 prefetch of the next wave's x columns, per degree (bit p): config 4 GDoF/s p7 34.1 -> 35.1, p8
+// 33.9 -> 34.4 (geometry on the fly: p7 32.2 -> 31.7, so not there; p8 33.1 -> 33.6); config 5 (p6)
+// 37.6 -> 36.6, so not at p6 (profiles/r02_ab_round2.md)
+#ifndef ELAS_FG_PFX_MASK
+#define ELAS_FG_PFX_MASK 0x180
+#endif
+template <int P> struct FgPfx { static constexpr bool value = ((ELAS_FG_PFX_MASK >> P) & 1) != 0; };
 #ifndef ELAS_FG_PADX_MASK
 #define ELAS_FG_PADX_MASK 0x20   // p5: 49 lines -> 64 per direction (config 4: 28.2 -> 30.9 GDoF/s at 4 CTAs/SM)
 #endif
@@ -333,6 +340,17 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qd + eid2 * (int64_t)C::QDE),
                    "r"((uint32_t)(C::QDE * sizeof(double)))
                    : "memory");
+    }
+  }
+  if constexpr (FgPfx<P>::value && (!OTF || P == 8)) {   // ... and its x columns (gather waits: 4-6 % of the samples at p7, p8)
+    const int64_t e2 = e + pf;
+    if (pf > 0 && e2 < e_end && zcol) {
+      int ex2, ey2, ez2;
+      coords(e2, ex2, ey2, ez2);
+      const double* xb2 = x + (int64_t)gc * s.nodes + (ex2 * P + gi) + (int64_t)s.Nx * (ey2 * P + gj) +
+                          plane * ((int64_t)ez2 * P);
+#pragma unroll
+      for (int k = 0; k < N; ++k) asm volatile("prefetch.global.L2 [%0];" ::"l"(xb2 + k * plane));
     }
   }
   __syncthreads();   // u gathered
