@@ -33,7 +33,9 @@ namespace elas {
 // wave's (p7 35.0 -> 34.4, p8 33.2 -> 32.4), L2 prefetch of the next wave's x columns (config 5
 // 37.6 -> 36.6), CTA sizes 256 at p6 (39.6 -> 38.4) and 288 at p7 (34.1 -> 34.0), p8 at 1 CTA/SM
 // (163 registers: 22.3 -> 20.5) and at 352 threads (120-byte spills), the gather with the
-// L2::256B hint (no change), interior plain stores (39.6 -> 37.6), persistent CTAs (spills).
+// L2::256B hint (no change), interior plain stores (39.6 -> 37.6), persistent CTAs (spills),
+// coefficients by per-thread LDC into general registers so the DFMAs avoid the uniform-register
+// operand (p6 39.6 -> 30.3, config 5 35.9 -> 29.7: one LDC per FMA and spills).
 // at most this many pointwise points' qdata in flight per thread (the rest loaded in-loop);
 // measured (config 4 GDoF/s, all / 3 / 2): p6 39.57 / 39.56 / 38.29, p7 34.10 / 34.08 / 33.70,
 // p8 33.15 / 33.31 / 33.85 (p8's 4-point prefetch spilled 28 bytes)
