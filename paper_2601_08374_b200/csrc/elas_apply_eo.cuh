@@ -989,10 +989,15 @@ template <int P> struct FgColored { static constexpr bool value = ELAS_FG_COLORE
                         // p5 27.7 -> 28.1, p6 33.6 -> 34.8, p7 24.3 -> 32.2, p8 30.0 -> 33.1; config 5 33.7 -> 34.8)
 #endif
 template <int P> struct FgOtf { static constexpr bool value = ELAS_FG_OTF != 0; };
+#ifndef ELAS_FG_ANISO
+#define ELAS_FG_ANISO 1   // anisotropic material (Eq. 2) on the fine-grained kernel too (config 4 GDoF/s
+                          // x-line -> FG: p5 26.0 -> 29.0, p6 31.3 -> 36.1, p7 23.8 -> 32.4, p8 27.3 -> 32.2)
+#endif
+template <int P> struct FgAniso { static constexpr bool value = ELAS_FG_ANISO != 0; };
 template <int P, int Q>
 cudaError_t launch_apply_fg(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
                             int64_t e_begin, int64_t e_end, cudaStream_t st, const ColorMap& cm, int otf,
-                            const double* tables);
+                            const double* tables, const double* cc);
 template <int P, int Q> void info_fg_pq(ApplyLaunch* info);
 
 template <int P, int Q, typename T>
@@ -1000,8 +1005,8 @@ cudaError_t launch_apply_eo_pq(const Slab& s, const double* x, double* y, const 
                                const void* tables, int64_t e_begin, int64_t e_end, cudaStream_t st,
                                const ColorMap& cm, int otf, const double* cc) {
   if constexpr (sizeof(T) == 8 && FgOn<P>::value) {
-    if (!cc && (!cm.on || FgColored<P>::value) && (!otf || FgOtf<P>::value))
-      return launch_apply_fg<P, Q>(s, x, y, qd, rr, e_begin, e_end, st, cm, otf, static_cast<const double*>(tables));
+    if ((!cc || FgAniso<P>::value) && (!cm.on || FgColored<P>::value) && (!otf || FgOtf<P>::value))
+      return launch_apply_fg<P, Q>(s, x, y, qd, rr, e_begin, e_end, st, cm, otf, static_cast<const double*>(tables), cc);
   }
   if constexpr (sizeof(T) == 8) {
     if (cc)

@@ -73,6 +73,7 @@ struct CfgFG {
   // geometry on the fly: Gauss points, sqrt weights and the element's trilinear-map words
   static constexpr int OFFG = TAB + ZE + YE;
   static constexpr size_t smem_otf = sizeof(double) * (size_t)(OFFG + 2 * Q + GEO_WORDS);
+  static constexpr size_t smem_aniso = sizeof(double) * (size_t)(OFFG + C21);   // the element's Voigt C
   static_assert(9 * Q * Q * OVN <= ZE, "gradient overflow must fit in the Z tile");
   static_assert(3 * N * N <= NT, "one z-column item per thread");
   static constexpr int QDE = qd_stride_words(Q, 8);
@@ -273,11 +274,11 @@ __device__ __forceinline__ void fg_otf_A(const double* __restrict__ gs, int Q, i
     for (int m = 0; m < 3; ++m) A[3 * d + m] = sc * adj[d][m];
 }
 
-template <int P, int Q, bool COLORED, bool OTF>
+template <int P, int Q, bool COLORED, bool OTF, bool ANISO = false>
 __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
     apply_fg_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
                     const double* __restrict__ rr, Slab s, int64_t e_begin, int64_t e_end, int pf, ColorMap cm,
-                    const double* __restrict__ tables) {
+                    const double* __restrict__ tables, const double* __restrict__ cc) {
   using C = CfgFG<P, Q>;
   using F = Fold<P, Q>;
   constexpr int N = C::N, NT = C::NT, QQ = Q * Q;
@@ -330,6 +331,9 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   const double* qe = qd + eid * (int64_t)C::QDE;
   const double r = __ldg(rr + eid);
   double* gsm = smem + C::OFFG;
+  if constexpr (ANISO) {   // the element's 21 Voigt words (Eq. 2), read in the pointwise stage
+    for (int t = tid; t < C21; t += NT) gsm[t] = cc[eid * C21 + t];
+  }
   if constexpr (OTF) {   // read only in the pointwise stage, several barriers later
     for (int t = tid; t < 2 * Q; t += NT) gsm[t] = tables[2 * Q * N + 2 * F::TS + t];
     for (int t = tid; t < GEO_WORDS; t += NT) gsm[2 * Q + t] = qd[eid * GEO_WORDS + t];
@@ -477,12 +481,14 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
         fg_otf_A(gsm, Q, a1, L / Q, L % Q, A);
         pointwise_t<double>(G, A, r);
       } else if (k < KPF) {
-        pointwise_t<double>(G, Ak[k < KPF ? k : 0], r);
+        if constexpr (ANISO) pointwise_aniso<double>(G, Ak[k < KPF ? k : 0], gsm);
+        else pointwise_t<double>(G, Ak[k < KPF ? k : 0], r);
       } else {
         double A[9];
 #pragma unroll
         for (int f = 0; f < 9; ++f) A[f] = qe[a1 * 9 * QQ + f * QQ + L];
-        pointwise_t<double>(G, A, r);
+        if constexpr (ANISO) pointwise_aniso<double>(G, A, gsm);
+        else pointwise_t<double>(G, A, r);
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c)
@@ -547,27 +553,30 @@ __global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P>::value)
   if (e0 < e_end) body(e0);
 }
 
-template <int P, int Q, bool COLORED, bool OTF>
+template <int P, int Q, bool COLORED, bool OTF, bool ANISO = false>
 cudaError_t launch_apply_fg_c(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
                               int64_t e_begin, int64_t e_end, cudaStream_t st, const ColorMap& cm,
-                              const double* tables) {
+                              const double* tables, const double* cc = nullptr) {
   using C = CfgFG<P, Q>;
-  constexpr size_t SMEM = OTF ? C::smem_otf : C::smem;
+  constexpr size_t SMEM = OTF ? C::smem_otf : ANISO ? C::smem_aniso : C::smem;
   static KernelPrep prep;
   int pref = 0;
-  cudaError_t err = prep.prep(apply_fg_kernel<P, Q, COLORED, OTF>, C::NT, SMEM, &pref);
+  cudaError_t err = prep.prep(apply_fg_kernel<P, Q, COLORED, OTF, ANISO>, C::NT, SMEM, &pref);
   if (err != cudaSuccess) return err;
   const int64_t ne = e_end - e_begin;
   if (ne <= 0) return cudaSuccess;
-  apply_fg_kernel<P, Q, COLORED, OTF><<<(unsigned)ne, C::NT, SMEM, st>>>(
-      x, y, static_cast<const double*>(qd), rr, s, e_begin, e_end, pref, cm, tables);
+  apply_fg_kernel<P, Q, COLORED, OTF, ANISO><<<(unsigned)ne, C::NT, SMEM, st>>>(
+      x, y, static_cast<const double*>(qd), rr, s, e_begin, e_end, pref, cm, tables, cc);
   return cudaGetLastError();
 }
 
 template <int P, int Q>
 cudaError_t launch_apply_fg(const Slab& s, const double* x, double* y, const void* qd, const double* rr,
                             int64_t e_begin, int64_t e_end, cudaStream_t st, const ColorMap& cm, int otf,
-                            const double* tables) {
+                            const double* tables, const double* cc) {
+  if (cc)
+    return cm.on ? launch_apply_fg_c<P, Q, true, false, true>(s, x, y, qd, rr, e_begin, e_end, st, cm, tables, cc)
+                 : launch_apply_fg_c<P, Q, false, false, true>(s, x, y, qd, rr, e_begin, e_end, st, cm, tables, cc);
   if (otf)
     return cm.on ? launch_apply_fg_c<P, Q, true, true>(s, x, y, qd, rr, e_begin, e_end, st, cm, tables)
                  : launch_apply_fg_c<P, Q, false, true>(s, x, y, qd, rr, e_begin, e_end, st, cm, tables);
