@@ -612,6 +612,56 @@ def test_launches_per_apply_matches_profiler():
         op.close()
 
 
+def test_kernel_family_per_degree_and_mode():
+    """Which kernel runs: the fine-grained FP64 kernel for p = 5..8 in the plain,
+    deterministic, geometry-on-the-fly and anisotropic modes; the folded x-line kernel for p = 2..4
+    and for the FP32 operator; each checked against the oracle on the same small mesh."""
+    torch = torch_mod()
+    import numpy as np
+    from paper_2601_08374_b200.elas import Operator, VARIANT_FOLDED_OTF, VARIANT_FOLDED_F32
+    from torch.profiler import profile, ProfilerActivity
+
+    def kernel_names(op, x, y):
+        op.apply(x, y)
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            op.apply(x, y)
+            torch.cuda.synchronize()
+        return [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
+                and "apply" in e.name]
+
+    for p in range(2, 9):
+        P = synth.make_problem("fam", 3, 2, 3, p, p + 2, perturb=True, lognormal_material=True, faces=1, seed=31 + p)
+        x = torch.from_numpy(P.x).cuda()
+        y = torch.empty_like(x)
+        ref = oracle.apply(oracle_mesh(P), P.x)
+        C6 = synth.random_C6(np.random.default_rng(p), (P.nz, P.ny, P.nx))
+        lam, mu = P.material_arrays()
+        ref_an = oracle.apply(oracle.Mesh(P.vertex_array(), P.p, P.q, lam, mu, P.dirichlet_faces, C6=C6), P.x)
+        modes = [("auto", lambda: Operator.from_problem(P), None, ref)]
+        if p >= 5:
+            modes += [("otf", lambda: Operator.from_problem(P, variant=VARIANT_FOLDED_OTF), None, ref),
+                      ("det", lambda: Operator.from_problem(P), "det", ref),
+                      ("aniso", lambda: Operator.anisotropic(P, C6), None, ref_an)]
+        for name, make, flag, want_y in modes:
+            op = make()
+            if flag == "det":
+                op.set_deterministic(True)
+            names = kernel_names(op, x, y)
+            want = "apply_fg_kernel" if p >= 5 else "apply_eo_kernel"
+            assert names and all(want in n for n in names), (p, name, names)
+            assert rel_l2(y.cpu().numpy(), want_y) <= TOL, (p, name)
+            op.close()
+    # FP32 operator: x-line kernel at every degree
+    P = synth.make_problem("fam32", 2, 2, 2, 6, 8, perturb=True, seed=5)
+    x = torch.from_numpy(P.x).cuda()
+    y = torch.empty_like(x)
+    op = Operator.from_problem(P, variant=VARIANT_FOLDED_F32)
+    names = kernel_names(op, x, y)
+    assert names and all("apply_eo_kernel" in n and "float" in n for n in names), names
+    op.close()
+
+
 # ---------------------------------------------------------------------------------------
 # general anisotropic material (Eq. 2)
 # ---------------------------------------------------------------------------------------
