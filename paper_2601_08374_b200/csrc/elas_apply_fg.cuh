@@ -78,9 +78,10 @@ struct CfgFG {
   static_assert(3 * N * N <= NT, "one z-column item per thread");
   static constexpr int QDE = qd_stride_words(Q, 8);
 };
-// CTAs per SM for the register cap.  p5 plain (no colors, stored isotropic qdata): 5 CTAs of 192
-// threads at 63 registers, spill-free (config 4: 30.85 -> 31.83 GDoF/s); the colored, on-the-fly
-// and anisotropic p5 instances spill at 64 registers and keep 4.  Measured and rejected at p4 (FG
+// CTAs per SM for the register cap.  p5 without colors and with isotropic material: 5 CTAs of 192
+// threads at 63-64 registers, spill-free at q = 7 (config 4: stored qdata 30.86 -> 31.82, geometry
+// on the fly 28.08 -> 29.42 GDoF/s); the colored and anisotropic p5 instances spill at 64
+// registers and keep 4.  Measured and rejected at p4 (FG
 // vs the x-line kernel's 28.5): 4 CTAs 25.3, 6 CTAs 26.6, 8 CTAs 26.3, X padded at 5 CTAs 24.0.
 template <int P, bool PLAIN = false> struct FgMinb {
   static constexpr int value = ELAS_FG_MINB > 0 ? ELAS_FG_MINB
@@ -280,7 +281,7 @@ __device__ __forceinline__ void fg_otf_A(const double* __restrict__ gs, int Q, i
 }
 
 template <int P, int Q, bool COLORED, bool OTF, bool ANISO = false>
-__global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P, !COLORED && !OTF && !ANISO>::value)
+__global__ void __launch_bounds__(CfgFG<P, Q>::NT, FgMinb<P, !COLORED && !ANISO>::value)
     apply_fg_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qd,
                     const double* __restrict__ rr, Slab s, int64_t e_begin, int64_t e_end, int pf, ColorMap cm,
                     const double* __restrict__ tables, const double* __restrict__ cc) {
